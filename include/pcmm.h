@@ -1,0 +1,187 @@
+/*
+ * pcmm.h -- C ABI of libpcmm.so: plaintext-ciphertext matrix multiplication
+ * (PC-MM) C = A . Enc(B) over EC-ElGamal on NIST P-256, on one NVIDIA B200
+ * (sm_100a), computed by Cussen's compression-reconstruction algorithm
+ * (schoolbook PC-MM as the comparison path).
+ *
+ * Source of every operation: arXiv 2504.14497 ("PAPER.md" line numbers):
+ *   KeyGen / Encrypt / Decrypt .......... Sec. 2.4
+ *   homomorphism (Eq. 5) ................ PAPER.md:186-193
+ *   schoolbook PC-MM .................... Sec. 3.1
+ *   Cussen vector-scalar (Alg. 2) ....... Sec. 3.2
+ *   proposed PC-MM (Alg. 3) ............. Sec. 3.3
+ *   curve P-256 ......................... Sec. 4.1
+ * Readings of the paper where it is silent (zero handling, pointer layout,
+ * signed plaintexts, wire format, ...) are listed in DESIGN.md (R1-R17).
+ *
+ * Conventions (all functions):
+ *   - Return an int status: PCMM_OK (0) or a negative PCMM_E* code; no C++
+ *     exception ever crosses the ABI.  pcmm_last_error() gives a message
+ *     (thread-local, valid until the next call on the same thread).
+ *   - Suffix _h = HOST pointer, _d = DEVICE pointer.  The caller allocates and
+ *     owns every buffer; the library never frees caller memory and never
+ *     retains a pointer after a call returns.
+ *   - Device work is enqueued on the given CUDA stream (a cudaStream_t passed
+ *     as void*; NULL = the legacy default stream) and is ASYNCHRONOUS unless a
+ *     function says otherwise.  Errors detected on the device (a plaintext out
+ *     of its w-bit range, an input point not on the curve) are recorded in the
+ *     workspace and returned by pcmm_status(), which synchronises the stream.
+ *   - Canonical ciphertext = 128 bytes C1 || C2; a point = 64 bytes x || y,
+ *     each coordinate 32-byte big-endian; the point at infinity is 64 zero
+ *     bytes ((0,0) is not on P-256).  Scalars are 32-byte big-endian.
+ *   - Matrices are row-major: A is m x n int8 (a_ik at A[i*n + k]); Enc(B)
+ *     is n x l canonical ciphertexts (b_kj at index k*l + j); outputs are
+ *     m x l (c_ij at index i*l + j).
+ *   - Signed plaintexts (is_signed = 1): a in [-2^(w-1), 2^(w-1)); a negative
+ *     a multiplies by the group element (q - |a|), i.e. -(|a| P) (DESIGN R10).
+ *     Unsigned: a in [0, 2^w).
+ *   - "Projective" outputs (ctC_proj_d) use an opaque-but-documented layout:
+ *     uint32 words [c in {C1,C2}][coord in {X,Y,Z}][limb 0..7][idx], count
+ *     = m*l points per component, Montgomery form (x*2^256 mod p),
+ *     homogeneous projective (x = X/Z, y = Y/Z, infinity <=> Z = 0).
+ *     Size in bytes: pcmm_proj_bytes(count) = 192 * count.
+ */
+#ifndef PCMM_H
+#define PCMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PCMM_API __attribute__((visibility("default")))
+#else
+#define PCMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCMM_OK 0
+#define PCMM_EINVAL (-1)       /* null pointer or invalid argument */
+#define PCMM_EDIM (-2)         /* a dimension <= 0, or too large */
+#define PCMM_EBOUND (-3)       /* a plaintext entry outside its w-bit range */
+#define PCMM_ENOTONCURVE (-4)  /* an input point not on P-256 / not reduced */
+#define PCMM_EDECODE (-5)      /* (per element) no message in [lo, hi] */
+#define PCMM_ECUDA (-6)        /* a CUDA runtime error */
+#define PCMM_ENOMEM (-7)       /* workspace too small / allocation failed */
+#define PCMM_ENOTSUP (-8)      /* parameters valid but not supported by this build */
+
+#define PCMM_PATH_SCHOOLBOOK 0
+#define PCMM_PATH_CUSSEN 1
+
+/* Message for the last error on this thread ("" if none). */
+PCMM_API const char *pcmm_last_error(void);
+
+/* Library version string. */
+PCMM_API const char *pcmm_version(void);
+
+/* Bytes of a projective output buffer for `count` ciphertexts (192 * count). */
+PCMM_API size_t pcmm_proj_bytes(int64_t count);
+
+/* KeyGen: x uniform in [1, q-1], H = x G.  x is drawn from
+ * SplitMix64(seed): 4 consecutive 64-bit draws concatenated big-endian,
+ * redrawn until in [1, q-1] (R12).  Writes sk_h = x (32 B BE) and
+ * pk_h = H (64 B canonical point).  SYNCHRONOUS (runs one small kernel on the
+ * current device's default stream and waits).  Errors: EINVAL, ECUDA.      */
+PCMM_API int pcmm_keygen(uint64_t seed, uint8_t sk_h[32], uint8_t pk_h[64]);
+
+/* Encrypt: ct[e] = (r_e G, r_e H + b_e G) for e < count.
+ *   pk_h : H, 64-byte canonical point (host; copied into the launch).
+ *   b_d  : int32[count] plaintexts (negative b means scalar q - |b|).
+ *   r_d  : uint8[count][32] big-endian randomness, each in [1, q-1] (caller's
+ *          responsibility; values are used as given).
+ *   ct_d : uint8[count][128] canonical ciphertexts (output).
+ * Errors: EINVAL (null / count < 0), ENOTONCURVE (pk not on curve), ECUDA. */
+PCMM_API int pcmm_encrypt(const uint8_t pk_h[64], const int32_t *b_d, const uint8_t *r_d, int64_t count, uint8_t *ct_d,
+                 void *stream);
+
+/* Workspace bytes needed by pcmm_mul_schoolbook (path 0) / pcmm_mul_cussen
+ * (path 1) / pcmm_normalize (path -1, m*l = count, n = l = 1) for these
+ * dimensions.  Returns 0 for invalid arguments.  The workspace must be device
+ * memory, 256-byte aligned, and must not be used concurrently by two calls. */
+PCMM_API size_t pcmm_workspace_bytes(int m, int n, int l, int w, int path);
+
+/* Schoolbook PC-MM: for every (i, j),
+ *   Enc(c_ij) = sum_k a_ik * Enc(b_kj)
+ * with one small-scalar multiplication (binary double-and-add) per term and
+ * complete projective additions.  Output: projective ctC_proj_d (m*l points
+ * per component, layout above).  w in [1, 8].  Async.
+ * Errors: EINVAL, EDIM, ENOMEM (ws_bytes too small), ECUDA; device-side
+ * EBOUND / ENOTONCURVE via pcmm_status(ws_d).                              */
+PCMM_API int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, int is_signed, const uint8_t *ctB_d,
+                        void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
+
+/* Cussen PC-MM (Alg. 3) with `iters` = N iterations of
+ * compression / reconstruction (the paper uses N = 4; 1 <= N <= 4 here):
+ *   a1  every column A[:,k] is compressed on the device (Alg. 2 lines 3-12):
+ *       sorted distinct nonzero values per level, differences, tracking
+ *       pointers, and the rank of each a_ik in level 1;
+ *   a2  per (k, j) the level-N values are multiplied by the ciphertext
+ *       (2 n_N small ECSMs, Alg. 3 line 5);
+ *   a3  reconstruction prefix sums (Alg. 2 lines 14-23) build the table
+ *       T_kj[v] = v * Enc(b_kj) for the distinct values v of A[:,k];
+ *   a4  un-sort / re-insert + accumulation (Alg. 3 lines 6-9): every output
+ *       gathers C_ij += T_kj[a_ik] from shared-memory table chunks.
+ * Output identical (after pcmm_normalize) to pcmm_mul_schoolbook.
+ * w in [1, 4] (tables of <= 15 entries per (k, j)).  Async.
+ * Errors as pcmm_mul_schoolbook; ENOTSUP for w > 4 or iters outside [1, 4]. */
+PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
+                    void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
+
+/* Normalise `count` projective ciphertexts (layout above, as written by
+ * pcmm_mul_*) to canonical affine bytes ctC_d[count][128] (x = X/Z, y = Y/Z,
+ * out of Montgomery form, big-endian; infinity -> 64 zero bytes), by
+ * Montgomery batch inversion.  Async.  Errors: EINVAL, ENOMEM, ECUDA.      */
+PCMM_API int pcmm_normalize(const void *ctC_proj_d, int64_t count, uint8_t *ctC_d, void *ws_d, size_t ws_bytes,
+                   void *stream);
+
+/* Decrypt: m_e = phi^-1(C2 - x C1) by an exact lookup in
+ * the table { m G : lo <= m <= hi } (hi - lo < 2^26).  sk_h = x (32 B BE).
+ * m_d[e] receives the message, status_d[e] = 0 or PCMM_EDECODE if no m in
+ * [lo, hi] matches (m_d[e] = 0 then) or PCMM_ENOTONCURVE for a bad input.
+ * Async (allocates its table stream-ordered on `stream`).
+ * Errors: EINVAL, ENOMEM, ECUDA.                                            */
+PCMM_API int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t count, int64_t lo, int64_t hi,
+                       int64_t *m_d, int32_t *status_d, void *stream);
+
+/* Synchronise `stream` and return the device-side status recorded in the
+ * workspace by the last pcmm_mul_* / pcmm_normalize call that used it:
+ * PCMM_OK, PCMM_EBOUND or PCMM_ENOTONCURVE (or ECUDA).                      */
+PCMM_API int pcmm_status(const void *ws_d, void *stream);
+
+/* ---- measurement hooks (used by bench.py; not needed for normal use) ---- */
+/* Enable (1) / disable (0) per-kernel CUDA-event timing of every launch made
+ * by the library; enabling clears the record.                              */
+PCMM_API int pcmm_profile_enable(int on);
+/* Synchronise the recorded events and copy out up to `max` records: kernel
+ * name (NUL-separated into names_h, 48 bytes per record) and duration in ms.
+ * Returns the number of records (or a negative status).                    */
+PCMM_API int pcmm_profile_read(char *names_h, float *ms_h, int max);
+
+/* ---- test hooks (unit parity tests of single steps) ---------------------- */
+/* Batched field ops on 32-byte big-endian values (reduced mod p):
+ * op 0 a+b, 1 a-b, 2 a*b, 3 a^-1, 4 -a (all mod p).  out_d[count][32].     */
+PCMM_API int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out_d, int64_t count, void *stream);
+/* Batched group ops on 64-byte canonical points: op 0 P+Q, 1 2P, 2 v*P
+ * (v_d[e], |v| < 2^15), 3 k*P (k = 32-byte BE scalar in q_d[e][0..31]).
+ * out_d[count][64].                                                          */
+PCMM_API int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_t *v_d, uint8_t *out_d,
+                    int64_t count, void *stream);
+/* The device compression plan of Alg. 2 (step a1) for every column of A:
+ * levels_d[n][4] = |a^(1)|..|a^(N)| (0 beyond N), sN_d[n][16] = values of the
+ * last level, rank_d[n][m] = 1 + index of a_ik in a^(1) (0 for a_ik = 0).
+ * Async; EBOUND via return after an internal synchronisation.              */
+PCMM_API int pcmm_test_plan(const int8_t *A_d, int m, int n, int w, int is_signed, int iters, int32_t *levels_d,
+                   int8_t *sN_d, uint8_t *rank_d, void *stream);
+/* fp_mul throughput probe: `blocks` x `threads` threads each run `iters`
+ * dependent-chain field multiplications on 4 independent chains; variant
+ * selects the fe_mul implementation (0 = library default).  Writes a
+ * checksum to out_d[blocks*threads][8].  Async.                             */
+PCMM_API int pcmm_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out_d, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCMM_H */

@@ -1,0 +1,417 @@
+// api.cu -- the C ABI of libpcmm.so (declared and documented in include/pcmm.h).
+// Host code only: argument validation, workspace carving, launch ordering on
+// the caller's stream, status reporting.  Every step of the PC-MM path runs in
+// the kernels of kernels.cu; nothing here computes on the host except keygen's
+// SplitMix64 draw of the secret scalar (R12).
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pcmm.h"
+#include "internal.h"
+
+using namespace pcmm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, const char *extra = nullptr) {
+    char buf[512];
+    snprintf(buf, sizeof buf, fmt, extra ? extra : "");
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    g_err = buf;
+    return PCMM_ECUDA;
+}
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---------------------------------------------------------------- profiling
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+// ---------------------------------------------------------------- workspace
+struct Layout {
+    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, partial = 0, total = 0;
+    int rows = 128, ksplit = 1;
+};
+
+Layout layout(int m, int n, int l, int path) {
+    Layout L;
+    size_t off = 256;                      // status word(s)
+    const size_t cnt = (size_t)n * l;
+    L.bsoa = off;
+    off = align256(off + cnt * 2 * kPtWords * 4);
+    if (path == PCMM_PATH_CUSSEN) {
+        L.rows = 128;                      // k_accum CTA = 128 rows (hot.cu kRows)
+        const int rowblocks = (m + L.rows - 1) / L.rows;
+        const int64_t base = (int64_t)l * 2 * rowblocks;
+        const int64_t target = 8LL * num_sms();            // enough CTAs to fill the chip
+        int ks = (int)((target + base - 1) / base);
+        if (ks > n) ks = n;
+        if (ks < 1) ks = 1;
+        L.ksplit = ks;
+        L.plans = off;
+        off = align256(off + (size_t)n * sizeof(ColPlan));
+        L.rank = off;
+        off = align256(off + (size_t)n * m);
+        L.tables = off;
+        off = align256(off + cnt * 2 * kTableWords * 4);
+        if (ks > 1) {
+            L.partial = off;
+            off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
+        }
+    }
+    L.total = off;
+    return L;
+}
+
+int check_dims(int m, int n, int l) {
+    if (m <= 0 || n <= 0 || l <= 0) return fail(PCMM_EDIM, "dimensions must be positive");
+    if ((int64_t)m * l > (1LL << 30) || (int64_t)n * l > (1LL << 30) || (int64_t)m * n > (1LL << 31))
+        return fail(PCMM_EDIM, "dimensions too large");
+    return PCMM_OK;
+}
+
+// SplitMix64 (Steele, Lea, Flood 2014) -- the counter-based generator of DESIGN.md R12
+struct SplitMix64 {
+    uint64_t s;
+    uint64_t next() {
+        s += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+};
+
+// group order q, big-endian 64-bit words
+const uint64_t kQ[4] = {0xffffffff00000000ULL, 0xffffffffffffffffULL, 0xbce6faada7179e84ULL, 0xf3b9cac2fc632551ULL};
+
+bool in_range_1_qm1(const uint64_t w[4]) {   // 1 <= w <= q - 1, w big-endian words
+    bool zero = (w[0] | w[1] | w[2] | w[3]) == 0;
+    if (zero) return false;
+    for (int i = 0; i < 4; i++) {
+        if (w[i] < kQ[i]) return true;
+        if (w[i] > kQ[i]) return false;
+    }
+    return false;                              // == q
+}
+
+}  // namespace
+
+namespace pcmm {
+
+void prof_begin(const char *name, cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    ProfRec r;
+    r.name = name;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    g_prof.push_back(r);
+}
+
+void prof_end(cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof.empty()) cudaEventRecord(g_prof.back().b, s);
+}
+
+}  // namespace pcmm
+
+#define LAUNCH(name, stream, call)                          \
+    do {                                                    \
+        prof_begin(name, stream);                           \
+        cudaError_t _e = (call);                            \
+        prof_end(stream);                                   \
+        if (_e != cudaSuccess) return cuda_fail(_e, name);  \
+    } while (0)
+
+extern "C" {
+
+const char *pcmm_last_error(void) { return g_err.c_str(); }
+
+const char *pcmm_version(void) { return "pcmm-b200 0.1 (sm_100a)"; }
+
+size_t pcmm_proj_bytes(int64_t count) { return count < 0 ? 0 : (size_t)count * 2 * kPtWords * 4; }
+
+size_t pcmm_workspace_bytes(int m, int n, int l, int w, int path) {
+    if (path == -1) return 256;
+    if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 8) return 0;
+    if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN) return 0;
+    return layout(m, n, l, path).total;
+}
+
+int pcmm_keygen(uint64_t seed, uint8_t sk_h[32], uint8_t pk_h[64]) {
+    g_err.clear();
+    if (!sk_h || !pk_h) return fail(PCMM_EINVAL, "null pointer");
+    SplitMix64 g{seed};
+    uint64_t w[4];
+    do {
+        for (int i = 0; i < 4; i++) w[i] = g.next();
+    } while (!in_range_1_qm1(w));
+    for (int i = 0; i < 4; i++)
+        for (int b = 0; b < 8; b++) sk_h[8 * i + b] = (uint8_t)(w[i] >> (56 - 8 * b));
+    uint32_t x[8];
+    for (int i = 0; i < 8; i++) {          // little-endian 32-bit words
+        const uint64_t word = w[3 - i / 2];
+        x[i] = (uint32_t)(i % 2 ? word >> 32 : word);
+    }
+    uint8_t *d = nullptr;
+    CK(cudaMalloc(&d, 64), "cudaMalloc");
+    cudaError_t e = launch_pubkey(x, d, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(pk_h, d, 64, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "keygen");
+    return PCMM_OK;
+}
+
+int pcmm_encrypt(const uint8_t pk_h[64], const int32_t *b_d, const uint8_t *r_d, int64_t count, uint8_t *ct_d,
+                 void *stream) {
+    g_err.clear();
+    if (count < 0) return fail(PCMM_EINVAL, "count < 0");
+    if (count == 0) return PCMM_OK;
+    if (!pk_h || !b_d || !r_d || !ct_d) return fail(PCMM_EINVAL, "null pointer");
+    bool zero = true;
+    for (int i = 0; i < 64; i++) zero = zero && pk_h[i] == 0;
+    if (zero) return fail(PCMM_ENOTONCURVE, "public key is the point at infinity");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("encrypt", s, launch_encrypt(pk_h, b_d, r_d, count, ct_d, s));
+    return PCMM_OK;
+}
+
+static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters,
+                      const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, cudaStream_t s) {
+    g_err.clear();
+    int rc = check_dims(m, n, l);
+    if (rc) return rc;
+    if (!A_d || !ctB_d || !ctC_proj_d || !ws_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)ctB_d & 15) || ((uintptr_t)ws_d & 255) || ((uintptr_t)ctC_proj_d & 15))
+        return fail(PCMM_EINVAL, "misaligned buffer (ctB/ctC 16 B, workspace 256 B)");
+    if (w < 1 || w > 8) return fail(PCMM_EINVAL, "w must be in [1, 8]");
+    if (path == PCMM_PATH_CUSSEN) {
+        if (w > 4) return fail(PCMM_ENOTSUP, "Cussen path supports w <= 4 in this build");
+        if (iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "iters must be in [1, 4]");
+    }
+    const Layout L = layout(m, n, l, path);
+    if (ws_bytes < L.total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_workspace_bytes)");
+    uint8_t *ws = (uint8_t *)ws_d;
+    int *status = (int *)ws;
+    uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
+    uint32_t *out = (uint32_t *)ctC_proj_d;
+    CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
+    LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
+    if (path == PCMM_PATH_SCHOOLBOOK) {
+        LAUNCH("schoolbook", s, launch_schoolbook(A_d, m, n, l, w, is_signed, bsoa, out, status, s));
+        return PCMM_OK;
+    }
+    ColPlan *plans = (ColPlan *)(ws + L.plans);
+    uint8_t *rank = ws + L.rank;
+    uint32_t *tables = (uint32_t *)(ws + L.tables);
+    LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
+    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, tables, s));
+    const int64_t cnt = (int64_t)m * l;
+    if (L.ksplit == 1) {
+        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.rows, 1, out, 0, s));
+    } else {
+        uint32_t *partial = (uint32_t *)(ws + L.partial);
+        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.rows, L.ksplit, partial, 2LL * kPtWords * cnt, s));
+        LAUNCH("reduce", s, launch_reduce_splits(partial, L.ksplit, cnt, out, s));
+    }
+    return PCMM_OK;
+}
+
+int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, int is_signed, const uint8_t *ctB_d,
+                        void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_common(PCMM_PATH_SCHOOLBOOK, A_d, m, n, l, w, is_signed, 0, ctB_d, ctC_proj_d, ws_d, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
+                    void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_common(PCMM_PATH_CUSSEN, A_d, m, n, l, w, is_signed, iters, ctB_d, ctC_proj_d, ws_d, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+int pcmm_normalize(const void *ctC_proj_d, int64_t count, uint8_t *ctC_d, void *ws_d, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    if (count < 0) return fail(PCMM_EINVAL, "count < 0");
+    if (count == 0) return PCMM_OK;
+    if (!ctC_proj_d || !ctC_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)ctC_d & 15)) return fail(PCMM_EINVAL, "misaligned output (16 B)");
+    (void)ws_d;
+    (void)ws_bytes;
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("normalize", s, launch_normalize((const uint32_t *)ctC_proj_d, count, ctC_d, s));
+    return PCMM_OK;
+}
+
+int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t count, int64_t lo, int64_t hi,
+                       int64_t *m_d, int32_t *status_d, void *stream) {
+    g_err.clear();
+    if (count < 0 || hi < lo) return fail(PCMM_EINVAL, "count < 0 or hi < lo");
+    if (hi - lo >= (1LL << 26) || lo <= -(1LL << 30) || hi >= (1LL << 30))
+        return fail(PCMM_EINVAL, "range too large (hi - lo < 2^26, |lo|, |hi| < 2^30)");
+    if (count == 0) return PCMM_OK;
+    if (!sk_h || !ct_d || !m_d || !status_d) return fail(PCMM_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t tc = hi - lo + 1;
+    uint32_t x[8];
+    for (int i = 0; i < 8; i++) {
+        const uint8_t *p = sk_h + 28 - 4 * i;
+        x[i] = ((uint32_t)p[0] << 24) | ((uint32_t)p[1] << 16) | ((uint32_t)p[2] << 8) | p[3];
+    }
+    size_t sort_tmp = 0;
+    CK(sort_pairs(nullptr, sort_tmp, nullptr, nullptr, nullptr, nullptr, tc, s), "sort sizing");
+    const size_t o_k0 = 0, o_k1 = align256(tc * 8), o_i0 = o_k1 + align256(tc * 8), o_i1 = o_i0 + align256(tc * 4),
+                 o_pts = o_i1 + align256(tc * 4), o_tmp = o_pts + align256(tc * 64), total = o_tmp + align256(sort_tmp);
+    uint8_t *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, total, s), "cudaMallocAsync");
+    uint64_t *k0 = (uint64_t *)(buf + o_k0), *k1 = (uint64_t *)(buf + o_k1);
+    uint32_t *i0 = (uint32_t *)(buf + o_i0), *i1 = (uint32_t *)(buf + o_i1);
+    uint8_t *pts = buf + o_pts;
+    int rc = PCMM_OK;
+    do {
+        prof_begin("dlog_table", s);
+        cudaError_t e = launch_dlog_table(lo, tc, k0, i0, pts, s);
+        prof_end(s);
+        if (e) { rc = cuda_fail(e, "dlog_table"); break; }
+        e = sort_pairs(buf + o_tmp, sort_tmp, k0, k1, i0, i1, tc, s);
+        if (e) { rc = cuda_fail(e, "sort"); break; }
+        prof_begin("decrypt", s);
+        e = launch_decrypt(x, ct_d, count, lo, k1, i1, pts, tc, m_d, status_d, s);
+        prof_end(s);
+        if (e) { rc = cuda_fail(e, "decrypt"); break; }
+    } while (0);
+    cudaFreeAsync(buf, s);
+    return rc;
+}
+
+int pcmm_status(const void *ws_d, void *stream) {
+    g_err.clear();
+    if (!ws_d) return fail(PCMM_EINVAL, "null workspace");
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = 0;
+    CK(cudaMemcpyAsync(&st, ws_d, 4, cudaMemcpyDeviceToHost, s), "status copy");
+    CK(cudaStreamSynchronize(s), "stream sync");
+    if (st & kStatusCurve) return fail(PCMM_ENOTONCURVE, "an input point is not on P-256 (or not reduced)");
+    if (st & kStatusBound) return fail(PCMM_EBOUND, "a plaintext entry is outside its w-bit range");
+    return PCMM_OK;
+}
+
+int pcmm_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    g_prof_on = on != 0;
+    return PCMM_OK;
+}
+
+int pcmm_profile_read(char *names_h, float *ms_h, int max) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    int n = 0;
+    for (auto &r : g_prof) {
+        if (n >= max) break;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "profile sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        if (names_h) {
+            strncpy(names_h + 48 * n, r.name, 47);
+            names_h[48 * n + 47] = 0;
+        }
+        if (ms_h) ms_h[n] = ms;
+        n++;
+    }
+    return n;
+}
+
+int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out_d, int64_t count, void *stream) {
+    g_err.clear();
+    if (count < 0 || op < 0 || op > 4) return fail(PCMM_EINVAL, "bad op / count");
+    if (count && (!a_d || !b_d || !out_d)) return fail(PCMM_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("test_field", s, launch_test_field(op, a_d, b_d, out_d, count, s));
+    return PCMM_OK;
+}
+
+int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_t *v_d, uint8_t *out_d,
+                    int64_t count, void *stream) {
+    g_err.clear();
+    if (count < 0 || op < 0 || op > 3) return fail(PCMM_EINVAL, "bad op / count");
+    if (count && (!p_d || !out_d || ((op == 0 || op == 3) && !q_d) || (op == 2 && !v_d)))
+        return fail(PCMM_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("test_point", s, launch_test_point(op, p_d, q_d, v_d, out_d, count, s));
+    return PCMM_OK;
+}
+
+int pcmm_test_plan(const int8_t *A_d, int m, int n, int w, int is_signed, int iters, int32_t *levels_d,
+                   int8_t *sN_d, uint8_t *rank_d, void *stream) {
+    g_err.clear();
+    int rc = check_dims(m, n, 1);
+    if (rc) return rc;
+    if (w < 1 || w > 4 || iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "w in [1,4], iters in [1,4]");
+    if (!A_d || !levels_d || !sN_d || !rank_d) return fail(PCMM_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    ColPlan *plans = nullptr;
+    int *status = nullptr;
+    const size_t status_off = align256((size_t)n * sizeof(ColPlan));
+    CK(cudaMallocAsync((void **)&plans, status_off + 256, s), "alloc");
+    status = (int *)((uint8_t *)plans + status_off);
+    cudaMemsetAsync(status, 0, 4, s);
+    cudaError_t e = launch_plan(A_d, m, n, w, is_signed, iters, plans, rank_d, status, s);
+    std::vector<ColPlan> hp(n);
+    int st = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp.data(), plans, (size_t)n * sizeof(ColPlan), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&st, status, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(plans, s);
+    if (e != cudaSuccess) return cuda_fail(e, "test_plan");
+    std::vector<int32_t> lev((size_t)n * 4);
+    std::vector<int8_t> sn((size_t)n * 16);
+    for (int k = 0; k < n; k++) {
+        for (int q = 0; q < 4; q++) lev[(size_t)k * 4 + q] = hp[k].n[q];
+        for (int q = 0; q < 16; q++) sn[(size_t)k * 16 + q] = hp[k].sN[q];
+    }
+    CK(cudaMemcpy(levels_d, lev.data(), lev.size() * 4, cudaMemcpyHostToDevice), "copy levels");
+    CK(cudaMemcpy(sN_d, sn.data(), sn.size(), cudaMemcpyHostToDevice), "copy sN");
+    if (st & kStatusBound) return fail(PCMM_EBOUND, "a plaintext entry is outside its w-bit range");
+    return PCMM_OK;
+}
+
+int pcmm_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out_d, void *stream) {
+    g_err.clear();
+    if (blocks <= 0 || threads <= 0 || threads > 128 || iters < 0 || !out_d) return fail(PCMM_EINVAL, "bad args");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("bench_fp_mul", s, launch_bench_fp_mul(variant, blocks, threads, iters, out_d, s));
+    return PCMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// ec.cuh -- NIST P-256 group law in homogeneous projective coordinates
+// (x = X/Z, y = Y/Z; identity = (0 : 1 : 0)) with the COMPLETE formulas of
+// Renes, Costello and Batina, "Complete addition formulas for prime order
+// elliptic curves" (EUROCRYPT 2016), Algorithm 4 (addition, a = -3,
+// 12M + 2m_b) and Algorithm 6 (doubling, a = -3, 8M + 3S + 2m_b).
+//
+// Completeness matters on this hot path: Cussen's prefix sums hit P + P
+// (2P = P + P) and zero plaintext entries add the identity
+// (R1), and both must be handled without branches.
+//
+// The group law, identity and ECSM are those of PAPER.md:150-155 (Sec. 2.3).
+#pragma once
+#include "fp.cuh"
+
+namespace pcmm {
+
+struct pt {
+    fe X, Y, Z;
+};
+
+PCMM_HD void pt_identity(pt &r) {
+    fe_zero(r.X);
+    fe_one_mont(r.Y);
+    fe_zero(r.Z);
+}
+
+PCMM_HD bool pt_is_identity(const pt &a) { return fe_is_zero(a.Z); }
+
+// RCB16 Algorithm 4: complete projective addition for a = -3.
+PCMM_HD void pt_add(pt &R, const pt &P, const pt &Q) {
+    fe t0, t1, t2, t3, t4, X3, Y3, Z3, b;
+    fe_b_mont(b);
+    fe_mul(t0, P.X, Q.X);
+    fe_mul(t1, P.Y, Q.Y);
+    fe_mul(t2, P.Z, Q.Z);
+    fe_add(t3, P.X, P.Y);
+    fe_add(t4, Q.X, Q.Y);
+    fe_mul(t3, t3, t4);
+    fe_add(t4, t0, t1);
+    fe_sub(t3, t3, t4);
+    fe_add(t4, P.Y, P.Z);
+    fe_add(X3, Q.Y, Q.Z);
+    fe_mul(t4, t4, X3);
+    fe_add(X3, t1, t2);
+    fe_sub(t4, t4, X3);
+    fe_add(X3, P.X, P.Z);
+    fe_add(Y3, Q.X, Q.Z);
+    fe_mul(X3, X3, Y3);
+    fe_add(Y3, t0, t2);
+    fe_sub(Y3, X3, Y3);
+    fe_mul(Z3, b, t2);
+    fe_sub(X3, Y3, Z3);
+    fe_add(Z3, X3, X3);
+    fe_add(X3, X3, Z3);
+    fe_sub(Z3, t1, X3);
+    fe_add(X3, t1, X3);
+    fe_mul(Y3, b, Y3);
+    fe_add(t1, t2, t2);
+    fe_add(t2, t1, t2);
+    fe_sub(Y3, Y3, t2);
+    fe_sub(Y3, Y3, t0);
+    fe_add(t1, Y3, Y3);
+    fe_add(Y3, t1, Y3);
+    fe_add(t1, t0, t0);
+    fe_add(t0, t1, t0);
+    fe_sub(t0, t0, t2);
+    fe_mul(t1, t4, Y3);
+    fe_mul(t2, t0, Y3);
+    fe_mul(Y3, X3, Z3);
+    fe_add(Y3, Y3, t2);
+    fe_mul(X3, t3, X3);
+    fe_sub(X3, X3, t1);
+    fe_mul(Z3, t4, Z3);
+    fe_mul(t1, t3, t0);
+    fe_add(Z3, Z3, t1);
+    R.X = X3;
+    R.Y = Y3;
+    R.Z = Z3;
+}
+
+// RCB16 Algorithm 6: complete projective doubling for a = -3.
+PCMM_HD void pt_dbl(pt &R, const pt &P) {
+    fe t0, t1, t2, t3, X3, Y3, Z3, b;
+    fe_b_mont(b);
+    fe_sqr(t0, P.X);
+    fe_sqr(t1, P.Y);
+    fe_sqr(t2, P.Z);
+    fe_mul(t3, P.X, P.Y);
+    fe_add(t3, t3, t3);
+    fe_mul(Z3, P.X, P.Z);
+    fe_add(Z3, Z3, Z3);
+    fe_mul(Y3, b, t2);
+    fe_sub(Y3, Y3, Z3);
+    fe_add(X3, Y3, Y3);
+    fe_add(Y3, X3, Y3);
+    fe_sub(X3, t1, Y3);
+    fe_add(Y3, t1, Y3);
+    fe_mul(Y3, X3, Y3);
+    fe_mul(X3, X3, t3);
+    fe_add(t3, t2, t2);
+    fe_add(t2, t2, t3);
+    fe_mul(Z3, b, Z3);
+    fe_sub(Z3, Z3, t2);
+    fe_sub(Z3, Z3, t0);
+    fe_add(t3, Z3, Z3);
+    fe_add(Z3, Z3, t3);
+    fe_add(t3, t0, t0);
+    fe_add(t0, t3, t0);
+    fe_sub(t0, t0, t2);
+    fe_mul(t0, t0, Z3);
+    fe_add(Y3, Y3, t0);
+    fe_mul(t0, P.Y, P.Z);
+    fe_add(t0, t0, t0);
+    fe_mul(Z3, t0, Z3);
+    fe_sub(X3, X3, Z3);
+    fe_mul(Z3, t0, t1);
+    fe_add(Z3, Z3, Z3);
+    fe_add(Z3, Z3, Z3);
+    R.X = X3;
+    R.Y = Y3;
+    R.Z = Z3;
+}
+
+// Out-of-line copies for the cold paths (table build, schoolbook ECSMs, encrypt,
+// decrypt): keeps compile time and code size bounded; the hot accumulate loop
+// uses the inlined forms above.
+PCMM_HD_NOINLINE void pt_add_nl(pt &R, const pt &P, const pt &Q) { pt_add(R, P, Q); }
+PCMM_HD_NOINLINE void pt_dbl_nl(pt &R, const pt &P) { pt_dbl(R, P); }
+
+PCMM_HD void pt_neg(pt &R, const pt &P) {
+    R.X = P.X;
+    fe_neg(R.Y, P.Y);
+    R.Z = P.Z;
+}
+
+// v * P for a small signed integer v (|v| < 2^15): left-to-right binary
+// double-and-add over the bits of |v|, then negation for v < 0 (R10:
+// -(|v| P) is the group element (q - |v|) P).  v = 0 gives the identity.
+PCMM_HD void pt_mul_small(pt &R, int v, const pt &P) {
+    unsigned a = v < 0 ? (unsigned)(-v) : (unsigned)v;
+    pt acc;
+    pt_identity(acc);
+    int top = 31;
+    while (top >= 0 && !((a >> top) & 1u)) top--;
+    for (int i = top; i >= 0; i--) {
+        if (i != top) pt_dbl_nl(acc, acc);
+        if ((a >> i) & 1u) {
+            if (i == top) acc = P;
+            else pt_add_nl(acc, acc, P);
+        }
+    }
+    if (v < 0) pt_neg(acc, acc);
+    R = acc;
+}
+
+// k * P for a 256-bit scalar k (8 little-endian 32-bit words), MSB-first
+// double-and-add with complete formulas (used by encrypt / keygen / decrypt,
+// not by the PC-MM hot path).
+PCMM_HD void pt_mul_scalar(pt &R, const uint32_t k[8], const pt &P) {
+    pt acc;
+    pt_identity(acc);
+    bool started = false;
+    for (int i = 255; i >= 0; i--) {
+        if (started) pt_dbl_nl(acc, acc);
+        if ((k[i >> 5] >> (i & 31)) & 1u) {
+            if (started) pt_add_nl(acc, acc, P);
+            else { acc = P; started = true; }
+        }
+    }
+    R = acc;
+}
+
+// (x, y) affine in Montgomery form -> projective with Z = 1
+PCMM_HD void pt_from_affine(pt &R, const fe &x, const fe &y) {
+    R.X = x;
+    R.Y = y;
+    fe_one_mont(R.Z);
+}
+
+// y^2 == x^3 - 3x + b (Montgomery form inputs)
+PCMM_HD bool affine_on_curve(const fe &x, const fe &y) {
+    fe y2, x3, t, b;
+    fe_sqr(y2, y);
+    fe_sqr(x3, x);
+    fe_mul(x3, x3, x);
+    fe_add(t, x, x);
+    fe_add(t, t, x);
+    fe_sub(x3, x3, t);
+    fe_b_mont(b);
+    fe_add(x3, x3, b);
+    return fe_eq(x3, y2);
+}
+
+// canonical 64-byte point (x||y big-endian, identity = 64 zero bytes) -> projective
+// Montgomery point.  Returns 0 ok, 1 if not on the curve / not reduced.
+PCMM_HD int pt_from_canonical(pt &R, const uint8_t *b64) {
+    uint32_t any = 0;
+    for (int i = 0; i < 64; i++) any |= b64[i];
+    if (any == 0) {
+        pt_identity(R);
+        return 0;
+    }
+    fe x, y;
+    int okx = fe_from_be_bytes(x, b64);
+    int oky = fe_from_be_bytes(y, b64 + 32);
+    fe_to_mont(x, x);
+    fe_to_mont(y, y);
+    pt_from_affine(R, x, y);
+    return (okx && oky && affine_on_curve(x, y)) ? 0 : 1;
+}
+
+// projective Montgomery point with known inverse zi = 1/Z (Montgomery) ->
+// canonical bytes; the identity (Z = 0) gives 64 zero bytes.
+PCMM_HD void pt_to_canonical_with_inv(uint8_t *b64, const pt &P, const fe &zi) {
+    if (pt_is_identity(P)) {
+        for (int i = 0; i < 64; i++) b64[i] = 0;
+        return;
+    }
+    fe x, y;
+    fe_mul(x, P.X, zi);
+    fe_mul(y, P.Y, zi);
+    fe_from_mont(x, x);
+    fe_from_mont(y, y);
+    fe_to_be_bytes(b64, x);
+    fe_to_be_bytes(b64 + 32, y);
+}
+
+PCMM_HD void pt_to_canonical(uint8_t *b64, const pt &P) {
+    fe zi;
+    fe_inv(zi, P.Z);
+    pt_to_canonical_with_inv(b64, P, zi);
+}
+
+}  // namespace pcmm

@@ -1,0 +1,66 @@
+// internal.h -- shared declarations between kernels.cu and api.cu (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace pcmm {
+
+// Per-column compression plan of Alg. 2 for w <= 4, N <= 4.
+// n[w-1] = |a^(w)| (sorted distinct nonzero values at level w, DESIGN R1);
+// sN = the level-N values (the multipliers of Alg. 3 line 5);
+// ptr[w-1][e] = index in a^(w+1) of element e of the differenced level-w vector
+// (the tracking pointer used by the un-sort / re-insert of level w+1 -> w).
+struct ColPlan {
+    int8_t n[4];
+    int8_t sN[16];
+    int8_t ptr[3][16];
+};
+
+constexpr int kMaxVals = 15;          // |a^(1)| <= 2^w - 1 for w <= 4 (signed: 15 nonzero values)
+constexpr int kSlots = 16;            // table slots per (k, j, c): slot 0 = infinity
+constexpr int kPtWords = 24;          // X, Y, Z x 8 limbs
+constexpr int kTableWords = kPtWords * kSlots;   // 384 words = 1536 B per (k, j, c)
+
+// status word bits (workspace offset 0)
+constexpr int kStatusBound = 1;
+constexpr int kStatusCurve = 2;
+
+struct Launch {
+    cudaStream_t stream;
+};
+
+// profiling (api.cu)
+void prof_begin(const char *name, cudaStream_t s);
+void prof_end(cudaStream_t s);
+
+// kernels.cu launchers; each returns cudaGetLastError()
+cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *status, cudaStream_t s);
+cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
+                        int *status, cudaStream_t s);
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, uint32_t *tables,
+                          cudaStream_t s);
+cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int rows, int ksplit,
+                         uint32_t *out, int64_t out_stride_split, cudaStream_t s);
+cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);
+cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
+                              uint32_t *out, int *status, cudaStream_t s);
+cudaError_t launch_normalize(const uint32_t *proj, int64_t count, uint8_t *ct, cudaStream_t s);
+cudaError_t launch_encrypt(const uint8_t *pk64, const int32_t *b, const uint8_t *r, int64_t count, uint8_t *ct,
+                           cudaStream_t s);
+cudaError_t launch_pubkey(const uint32_t x[8], uint8_t *out64_d, cudaStream_t s);
+cudaError_t launch_dlog_table(int64_t lo, int64_t count, uint64_t *keys, uint32_t *idx, uint8_t *pts,
+                              cudaStream_t s);
+cudaError_t launch_decrypt(const uint32_t x[8], const uint8_t *ct, int64_t count, int64_t lo, const uint64_t *keys,
+                           const uint32_t *idx, const uint8_t *pts, int64_t tcount, int64_t *m, int32_t *status,
+                           cudaStream_t s);
+cudaError_t sort_pairs(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
+                       uint32_t *vout, int64_t count, cudaStream_t s);
+cudaError_t launch_test_field(int op, const uint8_t *a, const uint8_t *b, uint8_t *out, int64_t count,
+                              cudaStream_t s);
+cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const int32_t *v, uint8_t *out,
+                              int64_t count, cudaStream_t s);
+cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s);
+int num_sms();
+
+}  // namespace pcmm

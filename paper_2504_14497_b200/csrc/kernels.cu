@@ -1,0 +1,621 @@
+// kernels.cu -- sm_100a kernels of the PC-MM hot path and of
+// the boundary calls around it.  Launched only through api.cu.
+//
+//   k_import       a0: canonical big-endian ciphertexts -> Montgomery SoA
+//   k_plan         a1: Alg. 2 compression of every column of A
+//   k_tables       a2+a3: per (k, j, component) ECSMs of the level-N values and
+//                  reconstruction prefix sums -> T_kj[v] = v * Enc(b_kj)
+//                  (Alg. 3 lines 5-6, Alg. 2 lines 13-23)
+//   k_accum        a4: un-sort / re-insert + accumulation C_ij += T_kj[a_ik]
+//                  from shared-memory table chunks (Alg. 3 lines 6-9)
+//   k_reduce       a5: split-k partial sums
+//   k_normalize    a6: batch inversion -> canonical affine bytes
+//   k_school       s1: schoolbook PC-MM
+//   k_encrypt / k_pubkey / k_dlog_table / k_decrypt: boundary
+#include <cub/device/device_radix_sort.cuh>
+
+#include "ec.cuh"
+#include "internal.h"
+
+namespace pcmm {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// 64 canonical bytes (x||y big-endian) -> 16 words as stored little-endian
+__device__ __forceinline__ void load64(const uint8_t *p, uint32_t w[16]) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(p);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        uint4 t = q[i];
+        w[4 * i + 0] = t.x; w[4 * i + 1] = t.y; w[4 * i + 2] = t.z; w[4 * i + 3] = t.w;
+    }
+}
+
+__device__ __forceinline__ void store64(uint8_t *p, const uint32_t w[16]) {
+    uint4 *q = reinterpret_cast<uint4 *>(p);
+#pragma unroll
+    for (int i = 0; i < 4; i++) q[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+}
+
+// canonical words -> (x, y) limbs (not reduced / not Montgomery); returns any-nonzero
+__device__ __forceinline__ uint32_t words_to_xy(const uint32_t w[16], fe &x, fe &y) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        x.v[i] = bswap32(w[7 - i]);
+        y.v[i] = bswap32(w[15 - i]);
+        any |= w[i] | w[8 + i];
+    }
+    return any;
+}
+
+__device__ __forceinline__ bool fe_lt_p(const fe &a) {
+    uint64_t borrow = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint64_t x = (uint64_t)a.v[i] - p_limb(i) - borrow;
+        borrow = (x >> 63) & 1;
+    }
+    return borrow != 0;
+}
+
+// canonical 64 bytes -> projective Montgomery point; returns false if invalid
+__device__ bool load_canonical_point(pt &P, const uint8_t *p) {
+    uint32_t w[16];
+    load64(p, w);
+    fe x, y;
+    if (words_to_xy(w, x, y) == 0) {
+        pt_identity(P);
+        return true;
+    }
+    bool ok = fe_lt_p(x) && fe_lt_p(y);
+    fe_to_mont(x, x);
+    fe_to_mont(y, y);
+    pt_from_affine(P, x, y);
+    return ok && affine_on_curve(x, y);
+}
+
+// affine (x, y) Montgomery -> canonical 64 bytes
+__device__ void store_canonical_xy(uint8_t *p, const fe &xm, const fe &ym) {
+    fe x, y;
+    fe_from_mont(x, xm);
+    fe_from_mont(y, ym);
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        w[7 - i] = bswap32(x.v[i]);
+        w[15 - i] = bswap32(y.v[i]);
+    }
+    store64(p, w);
+}
+
+__device__ void store_canonical_point(uint8_t *p, const pt &P) {
+    if (pt_is_identity(P)) {
+        uint32_t w[16] = {0};
+        store64(p, w);
+        return;
+    }
+    fe zi, x, y;
+    fe_inv(zi, P.Z);
+    fe_mul(x, P.X, zi);
+    fe_mul(y, P.Y, zi);
+    store_canonical_xy(p, x, y);
+}
+
+// SoA point access: base -> [coord][limb][stride]
+__device__ __forceinline__ void soa_load(pt &P, const uint32_t *base, int64_t stride, int64_t idx) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        P.X.v[i] = base[(0 * 8 + i) * stride + idx];
+        P.Y.v[i] = base[(1 * 8 + i) * stride + idx];
+        P.Z.v[i] = base[(2 * 8 + i) * stride + idx];
+    }
+}
+
+__device__ __forceinline__ void soa_store(uint32_t *base, int64_t stride, int64_t idx, const pt &P) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        base[(0 * 8 + i) * stride + idx] = P.X.v[i];
+        base[(1 * 8 + i) * stride + idx] = P.Y.v[i];
+        base[(2 * 8 + i) * stride + idx] = P.Z.v[i];
+    }
+}
+
+__device__ __forceinline__ void generator_mont(pt &G) {
+    G.X.v[0] = 0x18a9143cu; G.X.v[1] = 0x79e730d4u; G.X.v[2] = 0x5fedb601u; G.X.v[3] = 0x75ba95fcu;
+    G.X.v[4] = 0x77622510u; G.X.v[5] = 0x79fb732bu; G.X.v[6] = 0xa53755c6u; G.X.v[7] = 0x18905f76u;
+    G.Y.v[0] = 0xce95560au; G.Y.v[1] = 0xddf25357u; G.Y.v[2] = 0xba19e45cu; G.Y.v[3] = 0x8b4ab8e4u;
+    G.Y.v[4] = 0xdd21f325u; G.Y.v[5] = 0xd2e88688u; G.Y.v[6] = 0x25885d85u; G.Y.v[7] = 0x8571ff18u;
+    fe_one_mont(G.Z);
+}
+
+__device__ __forceinline__ void be32_to_words(const uint8_t *p, uint32_t k[8]) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(p);
+    uint4 a = q[0], b = q[1];
+    uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 8; i++) k[i] = bswap32(w[7 - i]);
+}
+
+// ------------------------------------------------------------ a0: import
+__global__ void k_import(const uint8_t *__restrict__ ct, int64_t count, uint32_t *__restrict__ soa,
+                         int *__restrict__ status) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * count) return;
+    int64_t e = t >> 1;
+    int c = (int)(t & 1);
+    pt P;
+    bool ok = load_canonical_point(P, ct + e * 128 + c * 64);
+    if (!ok) atomicOr(status, kStatusCurve);
+    soa_store(soa + (int64_t)c * kPtWords * count, count, e, P);
+}
+
+// ------------------------------------------------------------ a1: compression plan
+// One warp per column k of A.  Values of A lie in [-8, 15] (w <= 4), so the set
+// of distinct nonzero values of a column is a 24-bit presence mask (bit v+8).
+__global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is_signed, int N,
+                       ColPlan *__restrict__ plans, uint8_t *__restrict__ rank, int *__restrict__ status) {
+    int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int k = warp;
+    const int lo = is_signed ? -(1 << (w - 1)) : 0;
+    const int hi = is_signed ? (1 << (w - 1)) - 1 : (1 << w) - 1;
+    uint32_t mask = 0;
+    bool bad = false;
+    for (int i = lane; i < m; i += 32) {
+        int a = A[(int64_t)i * n + k];
+        if (a < lo || a > hi) bad = true;
+        else if (a != 0) mask |= 1u << (a + 8);
+    }
+    mask = __reduce_or_sync(0xffffffffu, mask);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, kStatusBound);
+    // rank[k][i] = 1 + index of a_ik in the sorted distinct nonzero values (0 for a_ik = 0)
+    for (int i = lane; i < m; i += 32) {
+        int a = A[(int64_t)i * n + k];
+        uint8_t r = 0;
+        if (a != 0 && a >= lo && a <= hi) r = (uint8_t)(1 + __popc(mask & ((1u << (a + 8)) - 1u)));
+        rank[(int64_t)k * m + i] = r;
+    }
+    if (lane != 0) return;
+    ColPlan P;
+#pragma unroll
+    for (int i = 0; i < 4; i++) P.n[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; i++) { P.sN[i] = 0; P.ptr[0][i] = 0; P.ptr[1][i] = 0; P.ptr[2][i] = 0; }
+    int s[16], v[16];
+    int ns = 0;
+    for (int b = 0; b < 24; b++)
+        if ((mask >> b) & 1u) s[ns++] = b - 8;                  // level 1: sorted distinct nonzero (R1)
+    for (int lev = 1; lev <= N; lev++) {
+        if (lev > 1) {
+            // sort the differenced vector v[0..nv) of level lev-1, dedupe -> s
+            int nv = ns;
+            int t[16];
+            for (int e = 0; e < nv; e++) t[e] = v[e];
+            for (int a = 1; a < nv; a++) {                      // insertion sort (<= 15 values)
+                int x = t[a], b2 = a - 1;
+                while (b2 >= 0 && t[b2] > x) { t[b2 + 1] = t[b2]; b2--; }
+                t[b2 + 1] = x;
+            }
+            ns = 0;
+            for (int e = 0; e < nv; e++)
+                if (ns == 0 || t[e] != s[ns - 1]) s[ns++] = t[e];
+            for (int e = 0; e < nv; e++) {                      // tracking pointers (R3)
+                int idx = 0;
+                while (s[idx] != v[e]) idx++;
+                P.ptr[lev - 2][e] = (int8_t)idx;
+            }
+        }
+        P.n[lev - 1] = (int8_t)ns;
+        if (lev < N) {                                          // differences, first element kept (R6)
+            for (int e = 0; e < ns; e++) v[e] = e == 0 ? s[0] : s[e] - s[e - 1];
+        } else {
+            for (int e = 0; e < ns; e++) P.sN[e] = (int8_t)s[e];
+        }
+    }
+    plans[k] = P;
+}
+
+// ------------------------------------------------------------ a2 + a3: tables
+// Thread per (component c, column k, output column j); j fastest so that the
+// loads of Enc(b_kj) are coalesced.  Reconstruction (Alg. 2 lines 14-23) in the
+// recursive form b^(w)[u] = b^(w)[u-1] + b^(w+1)[ptr^(w)[u]] (R3, R7).
+__global__ void k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans, int n, int l, int N,
+                         uint32_t *__restrict__ tables) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = 2LL * n * l;
+    if (t >= total) return;
+    const int j = (int)(t % l);
+    const int k = (int)((t / l) % n);
+    const int c = (int)(t / ((int64_t)l * n));
+    const int64_t cnt = (int64_t)n * l;
+    pt P;
+    soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
+    const ColPlan pl = plans[k];
+    pt cur[kMaxVals], nxt[kMaxVals];
+    int ncur = pl.n[N - 1];
+    for (int u = 0; u < ncur; u++) pt_mul_small(cur[u], pl.sN[u], P);     // Alg. 3 line 5
+    for (int lev = N - 1; lev >= 1; lev--) {
+        int nl = pl.n[lev - 1];
+        for (int u = 0; u < nl; u++) {
+            const pt &g = cur[pl.ptr[lev - 1][u]];
+            if (u == 0) nxt[0] = g;
+            else pt_add_nl(nxt[u], nxt[u - 1], g);                          // prefix sum
+        }
+        for (int u = 0; u < nl; u++) cur[u] = nxt[u];
+        ncur = nl;
+    }
+    uint32_t *dst = tables + (((int64_t)c * n + k) * l + j) * kTableWords;
+    pt id;
+    pt_identity(id);
+    for (int slot = 0; slot < kSlots; slot++) {
+        const pt &q = (slot >= 1 && slot <= ncur) ? cur[slot - 1] : id;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            dst[(0 * 8 + i) * kSlots + slot] = q.X.v[i];
+            dst[(1 * 8 + i) * kSlots + slot] = q.Y.v[i];
+            dst[(2 * 8 + i) * kSlots + slot] = q.Z.v[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------ a5: split-k reduce
+__global__ void k_reduce(const uint32_t *__restrict__ partial, int ksplit, int64_t count, uint32_t *__restrict__ out) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * count) return;
+    const int c = (int)(t / count);
+    const int64_t e = t % count;
+    const int64_t split_stride = 2LL * kPtWords * count;
+    pt acc, q;
+    soa_load(acc, partial + (int64_t)c * kPtWords * count, count, e);
+    for (int s = 1; s < ksplit; s++) {
+        soa_load(q, partial + s * split_stride + (int64_t)c * kPtWords * count, count, e);
+        pt_add_nl(acc, acc, q);
+    }
+    soa_store(out + (int64_t)c * kPtWords * count, count, e, acc);
+}
+
+// ------------------------------------------------------------ s1: schoolbook
+// lanes <-> output columns j (coalesced loads of Enc(b_kj)), warp <-> row i, so
+// a_ik is warp-uniform and the double-and-add control flow never diverges.
+__global__ void __launch_bounds__(128) k_school(const int8_t *__restrict__ A, int m, int n, int l, int w,
+                                               int is_signed, const uint32_t *__restrict__ bsoa,
+                                               uint32_t *__restrict__ out, int *__restrict__ status) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int jb = blockIdx.x, c = blockIdx.z;
+    const int i = blockIdx.y * 4 + warp;
+    if (i >= m) return;
+    const int j = jb * 32 + lane;
+    const int jj = min(j, l - 1);
+    const int lo = is_signed ? -(1 << (w - 1)) : 0;
+    const int hi = is_signed ? (1 << (w - 1)) - 1 : (1 << w) - 1;
+    const int64_t cnt = (int64_t)n * l;
+    const uint32_t *bc = bsoa + (int64_t)c * kPtWords * cnt;
+    pt acc, P, T;
+    pt_identity(acc);
+    bool bad = false;
+    for (int k = 0; k < n; k++) {
+        int v = A[(int64_t)i * n + k];
+        if (v < lo || v > hi) { bad = true; v = 0; }
+        if (v == 0) continue;                                  // 0 * ct = (inf, inf), warp-uniform
+        soa_load(P, bc, cnt, (int64_t)k * l + jj);
+        pt_mul_small(T, v, P);
+        pt_add_nl(acc, acc, T);
+    }
+    if (bad && lane == 0) atomicOr(status, kStatusBound);
+    if (j < l) {
+        const int64_t oc = (int64_t)m * l;
+        soa_store(out + (int64_t)c * kPtWords * oc, oc, (int64_t)i * l + j, acc);
+    }
+}
+
+// ------------------------------------------------------------ a6: normalise
+// Montgomery batch inversion over kBatch points per thread (3 fe_mul per point
+// + one inversion per batch); Z = 0 (infinity) is replaced by 1 in the batch.
+constexpr int kBatch = 8;
+
+__global__ void __launch_bounds__(128) k_normalize(const uint32_t *__restrict__ proj, int64_t count,
+                                                   uint8_t *__restrict__ ct) {
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = 2 * count;
+    fe pre[kBatch];
+    fe one;
+    fe_one_mont(one);
+    fe acc = one;
+    int nb = 0;
+#pragma unroll
+    for (int r = 0; r < kBatch; r++) {
+        const int64_t p = t + r * nthreads;
+        if (p < total) {
+            const int c = (int)(p / count);
+            const int64_t e = p % count;
+            fe z;
+#pragma unroll
+            for (int q = 0; q < 8; q++) z.v[q] = proj[(int64_t)c * kPtWords * count + (2 * 8 + q) * count + e];
+            if (fe_is_zero(z)) z = one;
+            fe_mul(acc, acc, z);
+            nb = r + 1;
+        }
+        pre[r] = acc;
+    }
+    if (nb == 0) return;
+    fe inv;
+    fe_inv(inv, pre[nb - 1]);
+#pragma unroll
+    for (int r = kBatch - 1; r >= 0; r--) {
+        if (r >= nb) continue;
+        const int64_t p = t + r * nthreads;
+        const int c = (int)(p / count);
+        const int64_t e = p % count;
+        pt P;
+        soa_load(P, proj + (int64_t)c * kPtWords * count, count, e);
+        fe zi;
+        if (r > 0) fe_mul(zi, inv, pre[r - 1]);
+        else zi = inv;
+        const bool isinf = fe_is_zero(P.Z);
+        if (r > 0) fe_mul(inv, inv, isinf ? one : P.Z);
+        uint8_t *dst = ct + e * 128 + c * 64;
+        if (isinf) {
+            uint32_t wz[16] = {0};
+            store64(dst, wz);
+        } else {
+            fe x, y;
+            fe_mul(x, P.X, zi);
+            fe_mul(y, P.Y, zi);
+            store_canonical_xy(dst, x, y);
+        }
+    }
+}
+
+// ------------------------------------------------------------ boundary kernels
+struct Pk64 {
+    uint8_t b[64];
+};
+
+__global__ void k_encrypt(const __grid_constant__ Pk64 pk, const int32_t *__restrict__ bvals, const uint8_t *__restrict__ r, int64_t count,
+                          uint8_t *__restrict__ ct) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    pt G, H, C1, C2, bG;
+    generator_mont(G);
+    uint8_t pkb[64];
+#pragma unroll
+    for (int i = 0; i < 64; i++) pkb[i] = pk.b[i];
+    pt_from_canonical(H, pkb);
+    uint32_t k[8];
+    be32_to_words(r + e * 32, k);
+    pt_mul_scalar(C1, k, G);                  // r G
+    pt_mul_scalar(C2, k, H);                  // r H
+    pt_mul_small(bG, bvals[e], G);            // phi(b) = b G
+    pt_add_nl(C2, C2, bG);
+    store_canonical_point(ct + e * 128, C1);
+    store_canonical_point(ct + e * 128 + 64, C2);
+}
+
+__global__ void k_pubkey(const uint32_t x0, const uint32_t x1, const uint32_t x2, const uint32_t x3,
+                         const uint32_t x4, const uint32_t x5, const uint32_t x6, const uint32_t x7,
+                         uint8_t *__restrict__ out) {
+    uint32_t k[8] = {x0, x1, x2, x3, x4, x5, x6, x7};
+    pt G, H;
+    generator_mont(G);
+    pt_mul_scalar(H, k, G);
+    store_canonical_point(out, H);
+}
+
+// table { m G : m = lo + t } with sort keys = first 8 bytes of the canonical bytes
+__global__ void k_dlog_table(int64_t lo, int64_t count, uint64_t *__restrict__ keys, uint32_t *__restrict__ idx,
+                             uint8_t *__restrict__ pts) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const int64_t mval = lo + t;
+    pt G, P;
+    generator_mont(G);
+    pt_mul_small(P, (int)mval, G);
+    uint8_t *dst = pts + t * 64;
+    store_canonical_point(dst, P);
+    const uint4 first = reinterpret_cast<const uint4 *>(dst)[0];
+    keys[t] = ((uint64_t)bswap32(first.x) << 32) | bswap32(first.y);
+    idx[t] = (uint32_t)t;
+}
+
+struct Scalar8 {
+    uint32_t k[8];
+};
+
+__global__ void k_decrypt(const __grid_constant__ Scalar8 x, const uint8_t *__restrict__ ct, int64_t count, int64_t lo,
+                          const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx,
+                          const uint8_t *__restrict__ pts, int64_t tcount, int64_t *__restrict__ mout,
+                          int32_t *__restrict__ status) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    pt C1, C2, M;
+    bool ok = load_canonical_point(C1, ct + e * 128);
+    ok = load_canonical_point(C2, ct + e * 128 + 64) && ok;
+    if (!ok) {
+        mout[e] = 0;
+        status[e] = -4;
+        return;
+    }
+    uint32_t xk[8];                            // local copy (never index the param space)
+#pragma unroll
+    for (int i = 0; i < 8; i++) xk[i] = x.k[i];
+    pt_mul_scalar(M, xk, C1);
+    pt_neg(M, M);
+    pt_add_nl(M, C2, M);                        // C2 - x C1 = phi(m)
+    __align__(16) uint8_t buf[64];
+    store_canonical_point(buf, M);
+    const uint4 first = reinterpret_cast<const uint4 *>(buf)[0];
+    const uint64_t key = ((uint64_t)bswap32(first.x) << 32) | bswap32(first.y);
+    int64_t a = 0, b = tcount;                 // lower bound of key
+    while (a < b) {
+        int64_t mid = (a + b) >> 1;
+        if (keys[mid] < key) a = mid + 1;
+        else b = mid;
+    }
+    int32_t st = -5;
+    int64_t mv = 0;
+    for (int64_t q = a; q < tcount && keys[q] == key; q++) {
+        const uint4 *cand = reinterpret_cast<const uint4 *>(pts + (int64_t)idx[q] * 64);
+        const uint4 *mine = reinterpret_cast<const uint4 *>(buf);
+        bool eq = true;
+#pragma unroll
+        for (int z = 0; z < 4; z++) {
+            uint4 u = cand[z], v = mine[z];
+            eq = eq && u.x == v.x && u.y == v.y && u.z == v.z && u.w == v.w;
+        }
+        if (eq) {
+            st = 0;
+            mv = lo + idx[q];
+            break;
+        }
+    }
+    mout[e] = mv;
+    status[e] = st;
+}
+
+// ------------------------------------------------------------ test hooks
+__global__ void k_test_field(int op, const uint8_t *__restrict__ a, const uint8_t *__restrict__ b,
+                             uint8_t *__restrict__ out, int64_t count) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    fe x, y, r;
+    fe_from_be_bytes(x, a + e * 32);
+    fe_from_be_bytes(y, b + e * 32);
+    fe_to_mont(x, x);
+    fe_to_mont(y, y);
+    switch (op) {
+        case 0: fe_add(r, x, y); break;
+        case 1: fe_sub(r, x, y); break;
+        case 2: fe_mul(r, x, y); break;
+        case 3: fe_inv(r, x); break;
+        default: fe_neg(r, x); break;
+    }
+    fe_from_mont(r, r);
+    fe_to_be_bytes(out + e * 32, r);
+}
+
+__global__ void k_test_point(int op, const uint8_t *__restrict__ p, const uint8_t *__restrict__ q,
+                             const int32_t *__restrict__ v, uint8_t *__restrict__ out, int64_t count) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    pt P, Q, R;
+    load_canonical_point(P, p + e * 64);
+    if (op == 0) {
+        load_canonical_point(Q, q + e * 64);
+        pt_add_nl(R, P, Q);
+    } else if (op == 1) {
+        pt_dbl_nl(R, P);
+    } else if (op == 2) {
+        pt_mul_small(R, v[e], P);
+    } else {
+        uint32_t k[8];
+        be32_to_words(q + e * 64, k);
+        pt_mul_scalar(R, k, P);
+    }
+    store_canonical_point(out + e * 64, R);
+}
+
+// ------------------------------------------------------------ launchers
+static inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *status, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_import<<<blocks_for(2 * count, 128), 128, 0, s>>>(ct, count, soa, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
+                        int *status, cudaStream_t s) {
+    k_plan<<<blocks_for((int64_t)n * 32, 128), 128, 0, s>>>(A, m, n, w, is_signed, N, plans, rank, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, uint32_t *tables,
+                          cudaStream_t s) {
+    k_tables<<<blocks_for(2LL * n * l, 64), 64, 0, s>>>(bsoa, plans, n, l, N, tables);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s) {
+    k_reduce<<<blocks_for(2 * count, 128), 128, 0, s>>>(partial, ksplit, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
+                              uint32_t *out, int *status, cudaStream_t s) {
+    dim3 grid((unsigned)((l + 31) / 32), (unsigned)((m + 3) / 4), 2);
+    k_school<<<grid, 128, 0, s>>>(A, m, n, l, w, is_signed, bsoa, out, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(const uint32_t *proj, int64_t count, uint8_t *ct, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    const int64_t threads = (2 * count + kBatch - 1) / kBatch;
+    k_normalize<<<blocks_for(threads, 128), 128, 0, s>>>(proj, count, ct);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encrypt(const uint8_t *pk64, const int32_t *b, const uint8_t *r, int64_t count, uint8_t *ct,
+                           cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    Pk64 pk;
+    for (int i = 0; i < 64; i++) pk.b[i] = pk64[i];
+    k_encrypt<<<blocks_for(count, 64), 64, 0, s>>>(pk, b, r, count, ct);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pubkey(const uint32_t x[8], uint8_t *out64_d, cudaStream_t s) {
+    k_pubkey<<<1, 1, 0, s>>>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], out64_d);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dlog_table(int64_t lo, int64_t count, uint64_t *keys, uint32_t *idx, uint8_t *pts,
+                              cudaStream_t s) {
+    k_dlog_table<<<blocks_for(count, 128), 128, 0, s>>>(lo, count, keys, idx, pts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decrypt(const uint32_t x[8], const uint8_t *ct, int64_t count, int64_t lo, const uint64_t *keys,
+                           const uint32_t *idx, const uint8_t *pts, int64_t tcount, int64_t *m, int32_t *status,
+                           cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    Scalar8 xs;
+    for (int i = 0; i < 8; i++) xs.k[i] = x[i];
+    k_decrypt<<<blocks_for(count, 64), 64, 0, s>>>(xs, ct, count, lo, keys, idx, pts, tcount, m, status);
+    return cudaGetLastError();
+}
+
+cudaError_t sort_pairs(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
+                       uint32_t *vout, int64_t count, cudaStream_t s) {
+    return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)count, 0, 64, s);
+}
+
+cudaError_t launch_test_field(int op, const uint8_t *a, const uint8_t *b, uint8_t *out, int64_t count,
+                              cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_test_field<<<blocks_for(count, 128), 128, 0, s>>>(op, a, b, out, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const int32_t *v, uint8_t *out,
+                              int64_t count, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_test_point<<<blocks_for(count, 64), 64, 0, s>>>(op, p, q, v, out, count);
+    return cudaGetLastError();
+}
+
+}  // namespace pcmm

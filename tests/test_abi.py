@@ -1,0 +1,62 @@
+"""CPU checks of the boundary: libpcmm.so builds for sm_100a, loads without a GPU,
+and exports every symbol include/pcmm.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+import shutil
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pcmm.h")).read()
+    return sorted(set(re.findall(r"PCMM_API\s+[\w\s\*]*?\b(pcmm_\w+)\s*\(", src)))
+
+
+@pytest.mark.skipif(shutil.which("nvcc") is None, reason="nvcc not available")
+def test_library_exports_every_declared_symbol():
+    from paper_2504_14497_b200 import build, pcmm
+    build.build()
+    lib = ctypes.CDLL(build.LIB)
+    names = _declared()
+    assert len(names) >= 17
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(pcmm.EXPORTS)
+    lib.pcmm_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.pcmm_version()
+
+
+@pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
+def test_library_is_sm100a_only():
+    import subprocess
+    from paper_2504_14497_b200 import build
+    build.build()
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2504_14497_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_validation_without_gpu():
+    # argument errors are detected on the host before any device work
+    from paper_2504_14497_b200 import pcmm
+    L = pcmm.load()
+    assert L.pcmm_workspace_bytes(0, 4, 4, 4, 1) == 0
+    assert L.pcmm_workspace_bytes(4, 4, 4, 9, 1) == 0
+    assert L.pcmm_workspace_bytes(4, 4, 4, 4, 1) > 0
+    rc = L.pcmm_mul_cussen(None, 0, 4, 4, 4, 0, 4, None, None, None, 0, None)
+    assert rc == pcmm.PCMM_EDIM
+    rc = L.pcmm_mul_cussen(None, 4, 4, 4, 4, 0, 4, None, None, None, 0, None)
+    assert rc == pcmm.PCMM_EINVAL
+    assert L.pcmm_last_error()

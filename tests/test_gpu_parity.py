@@ -1,0 +1,260 @@
+"""GPU parity tests: the CUDA path through the C ABI vs the CPU oracle (oracle/).
+
+Bar (north_star): BIT-EXACT canonical affine bytes for every output
+compared -- all of this is integer work, there is no tolerance.  Expected values
+come only from `oracle/` (and, for scalar multiples, OpenSSL via tests/ecref.py)
+applied to the seeded synthetic inputs of `synth`; never from the CUDA path.
+
+* small configs (tiny, 64^3, ragged shapes): every output, oracle-encrypted inputs;
+* full BASELINE sizes (256^3, 512^3, ML): the launch configuration bench.py uses,
+  inputs encrypted on the GPU (that encryption is itself checked on a sample
+  against the oracle), outputs checked on a sample against the Eq. 5 closed form
+  evaluated by the oracle from (x, A, B, r) alone.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import ecref
+
+pytestmark = pytest.mark.gpu
+
+P = None
+
+
+def setup_module(_m):
+    global P
+    from paper_2504_14497_b200 import pcmm
+    P = pcmm
+    P.load()
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+rng = random.Random(1234)
+
+
+# ------------------------------------------------------------------ field / points
+def test_field_ops_bit_exact():
+    vals = [0, 1, 2, ecref.P - 1, ecref.P - 2, 2**224, 2**96 - 1] + [rng.randrange(ecref.P) for _ in range(4000)]
+    a = vals
+    b = [rng.choice(vals) for _ in vals]
+    A = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in a), dtype=np.uint8).reshape(-1, 32))
+    B = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in b), dtype=np.uint8).reshape(-1, 32))
+    for op, f in [(0, lambda x, y: (x + y) % ecref.P), (1, lambda x, y: (x - y) % ecref.P),
+                  (2, lambda x, y: x * y % ecref.P), (4, lambda x, y: (-x) % ecref.P)]:
+        out = P.test_field(op, A, B).cpu().numpy()
+        for i in range(len(a)):
+            assert int.from_bytes(out[i].tobytes(), "big") == f(a[i], b[i]), (op, i)
+    out = P.test_field(3, A, B).cpu().numpy()
+    for i in range(len(a)):
+        exp = pow(a[i], -1, ecref.P) if a[i] else 0
+        assert int.from_bytes(out[i].tobytes(), "big") == exp
+
+
+def _pts(scalars):
+    return cuda(np.frombuffer(b"".join(ecref.mulG(s) for s in scalars), dtype=np.uint8).reshape(-1, 64))
+
+
+def test_point_ops_vs_openssl():
+    n = 64
+    a = [rng.randrange(1, ecref.Q) for _ in range(n)]
+    b = [rng.randrange(1, ecref.Q) for _ in range(n)]
+    b[0], b[1], b[2] = a[0], ecref.Q - a[1], 0           # P+P, P+(-P), P+inf through the add formula
+    a[3] = 0                                               # inf + Q
+    Pa, Pb = _pts(a), _pts(b)
+    add = P.test_point(0, Pa, Pb).cpu().numpy()
+    dbl = P.test_point(1, Pa).cpu().numpy()
+    v = [rng.randrange(-40000, 40000) for _ in range(n)]
+    v[4], v[5] = 0, 1
+    mul = P.test_point(2, Pa, v=cuda(np.array(v, dtype=np.int32))).cpu().numpy()
+    k = [rng.randrange(2**256) for _ in range(n)]
+    K = cuda(np.frombuffer(b"".join(x.to_bytes(32, "big") + bytes(32) for x in k), dtype=np.uint8).reshape(-1, 64))
+    kmul = P.test_point(3, Pa, K).cpu().numpy()
+    for i in range(n):
+        assert add[i].tobytes() == ecref.mulG(a[i] + b[i]), i
+        assert dbl[i].tobytes() == ecref.mulG(2 * a[i]), i
+        assert mul[i].tobytes() == ecref.mulG(v[i] * a[i]), i
+        assert kmul[i].tobytes() == ecref.mulG(k[i] * a[i]), i
+
+
+# ------------------------------------------------------------------ EC-ElGamal boundary
+def test_keygen_matches_generator_and_openssl():
+    for seed in (0, 1, 2, 3, 4, 12345):
+        sk, pk = P.keygen(seed)
+        x = synth.keygen_secret(seed)
+        assert int.from_bytes(sk, "big") == x
+        assert pk == ecref.mulG(x) == oracle.pubkey(x)
+
+
+def test_encrypt_matches_oracle():
+    I = synth.make_instance(synth.CONFIGS["c64"], m=4, n=16, l=16, seed=77)
+    sk, pk = P.keygen(77)
+    b = I.B.reshape(-1).astype(np.int32)
+    b[:4] = [0, 1, -1, -255]
+    ct = P.encrypt(pk, cuda(b), cuda(I.r_be)).cpu().numpy()
+    exp = oracle.encrypt(pk, b.astype(np.int64), I.r_be)
+    assert (ct == exp).all()
+
+
+def test_decrypt_small():
+    I = synth.make_instance(synth.CONFIGS["c64"], m=4, n=8, l=8, seed=5)
+    sk, pk = P.keygen(5)
+    b = np.arange(-20, 44, dtype=np.int32)
+    ct = oracle.encrypt(pk, b.astype(np.int64), I.r_be[:64])
+    m, st = P.decrypt_small(sk, cuda(ct), -20, 43)
+    assert (st.cpu().numpy() == 0).all() and (m.cpu().numpy() == b).all()
+    m, st = P.decrypt_small(sk, cuda(ct), 0, 10)
+    st = st.cpu().numpy()
+    assert ((st == P.PCMM_EDECODE) == ((b < 0) | (b > 10))).all()
+
+
+# ------------------------------------------------------------------ step a1: compression plan
+@pytest.mark.parametrize("w,signed", [(1, False), (2, False), (3, False), (4, False), (4, True), (2, True)])
+def test_plan_matches_oracle(w, signed):
+    g = np.random.default_rng(w * 10 + signed)
+    lo, hi = (-(1 << (w - 1)), (1 << (w - 1)) - 1) if signed else (0, (1 << w) - 1)
+    m, n = 77, 40
+    A = g.integers(lo, hi + 1, (m, n)).astype(np.int8)
+    A[:, 0] = 0                                   # all-zero column
+    A[:, 1] = hi                                  # constant column
+    A[::3, 2] = 0                                 # many zeros
+    for N in (1, 2, 3, 4):
+        levels, sN, rank = P.test_plan(cuda(A), w, signed, N)
+        levels, sN, rank = levels.cpu().numpy(), sN.cpu().numpy(), rank.cpu().numpy()
+        for k in range(n):
+            lev = oracle.cussen_plan(A[:, k].astype(np.int64), N)
+            assert list(levels[k, :N]) == [len(s) for s, _ in lev], (N, k)
+            assert list(sN[k, : len(lev[-1][0])]) == list(lev[-1][0])
+            exp_rank = np.where(lev[0][1] < 0, 0, lev[0][1] + 1)
+            assert (rank[k] == exp_rank).all()
+
+
+# ------------------------------------------------------------------ full PC-MM, small sizes: every output
+def _gpu_pcmm(A, ct, l, w, signed, path, iters=4):
+    return P.pcmm(cuda(A), cuda(ct), l, w, signed, path=path, iters=iters).cpu().numpy()
+
+
+def test_tiny_config_both_paths_and_decrypt():
+    I = synth.make_instance(synth.CONFIGS["tiny"])
+    sk, pk = P.keygen(0)
+    ct = oracle.encrypt(pk, I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, 8, 2)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        out = _gpu_pcmm(I.A, ct, 8, 2, False, path)
+        assert (out == exp).all(), path
+    # P6: brute-force dlog of the GPU output = A.B
+    m, st = P.decrypt_small(sk, cuda(exp), 0, 72)
+    assert (st.cpu().numpy() == 0).all()
+    assert (m.cpu().numpy().reshape(8, 8) == I.A.astype(np.int64) @ I.B.astype(np.int64)).all()
+
+
+def test_tiny_forced_real_ecsm_column():
+    # force a column whose compression ends in a value != 1 (a real ECSM, step a2)
+    I = synth.make_instance(synth.CONFIGS["tiny"])
+    A = I.A.copy()
+    A[:, 3] = [0, 3, 3, 0, 3, 0, 0, 3]            # level values {3} -> ECSM by 3
+    A[:, 5] = [2, 0, 2, 2, 0, 0, 2, 0]            # {2}
+    sk, pk = P.keygen(0)
+    ct = oracle.encrypt(pk, I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.SCHOOLBOOK, A, ct, 8, 2)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(A, ct, 8, 2, False, path) == exp).all()
+
+
+def test_c64_config_every_output():
+    I = synth.make_instance(synth.CONFIGS["c64"])
+    sk, pk = P.keygen(1)
+    ct = oracle.encrypt(pk, I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, 64, 4)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(I.A, ct, 64, 4, False, path) == exp).all(), path
+
+
+@pytest.mark.parametrize("shape,w,signed,iters", [((100, 37, 45), 3, True, 4), ((129, 70, 33), 4, False, 4),
+                                                  ((1, 1, 1), 4, False, 4), ((1, 200, 3), 4, True, 2),
+                                                  ((260, 5, 1), 2, False, 1), ((33, 64, 130), 4, True, 3)])
+def test_ragged_shapes_every_output(shape, w, signed, iters):
+    m, n, l = shape
+    cfg = synth.Config("ragged", m, n, l, w, signed, 0, 255, 1000 + m)
+    I = synth.make_instance(cfg)
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.SCHOOLBOOK if n * m * l < 20000 else oracle.CUSSEN, I.A, ct, l, w)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(I.A, ct, l, w, signed, path, iters) == exp).all(), path
+
+
+def test_degenerate_matrices():
+    I = synth.make_instance(synth.CONFIGS["c64"], m=16, n=16, l=8, seed=9)
+    x = synth.keygen_secret(9)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    Z = np.zeros((16, 16), dtype=np.int8)
+    E = np.eye(16, dtype=np.int8)
+    C = np.full((16, 16), 15, dtype=np.int8)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(Z, ct, 8, 4, False, path) == 0).all()                 # (inf, inf)
+        assert (_gpu_pcmm(E, ct, 8, 4, False, path) == ct).all()                # A = I -> Enc(B)
+        exp, _ = oracle.pcmm(oracle.CUSSEN, C, ct, 8, 4)
+        assert (_gpu_pcmm(C, ct, 8, 4, False, path) == exp).all()
+    # an infinity ciphertext in the input
+    ct2 = ct.copy()
+    ct2[5] = 0
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct2, 8, 4)
+    assert (_gpu_pcmm(I.A, ct2, 8, 4, False, P.CUSSEN) == exp).all()
+
+
+def test_error_reporting():
+    I = synth.make_instance(synth.CONFIGS["c64"], m=8, n=8, l=8, seed=3)
+    x = synth.keygen_secret(3)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    bad = I.A.copy()
+    bad[2, 3] = 16
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        with pytest.raises(P.PCMMError) as e:
+            _gpu_pcmm(bad, ct, 8, 4, False, path)
+        assert e.value.code == P.PCMM_EBOUND
+    cbad = ct.copy()
+    cbad[7, 10] ^= 1
+    with pytest.raises(P.PCMMError) as e:
+        _gpu_pcmm(I.A, cbad, 8, 4, False, P.CUSSEN)
+    assert e.value.code == P.PCMM_ENOTONCURVE
+    with pytest.raises(P.PCMMError) as e:
+        _gpu_pcmm(I.A, ct, 8, 5, False, P.CUSSEN)
+    assert e.value.code == P.PCMM_ENOTSUP
+
+
+# ------------------------------------------------------------------ full BASELINE sizes: sampled outputs
+def _full_size(name, path, samples):
+    cfg = synth.CONFIGS[name]
+    I = synth.make_instance(cfg)
+    sk, pk = P.keygen(cfg.seed)
+    n, l = cfg.n, cfg.l
+    ctd = P.encrypt(pk, cuda(I.B.reshape(-1).astype(np.int32)), cuda(I.r_be))
+    ct = ctd.cpu().numpy()
+    g = np.random.default_rng(cfg.seed)
+    idx = g.choice(n * l, 24, replace=False)
+    exp_ct = oracle.encrypt(pk, I.B.reshape(-1)[idx].astype(np.int64), I.r_be[idx])
+    assert (ct[idx] == exp_ct).all()                                  # GPU encryption vs oracle
+    out = P.pcmm(cuda(I.A), ctd, l, cfg.w, cfg.signed, path=path).cpu().numpy()
+    r = I.r_be.reshape(n, l, 32)
+    picks = [(0, 0), (cfg.m - 1, l - 1)] + [(int(g.integers(cfg.m)), int(g.integers(l))) for _ in range(samples)]
+    for (i, j) in picks:
+        exp = oracle.closed_form(I.x, I.A[i], I.B[:, j], r[:, j])
+        assert out[i * l + j].tobytes() == exp, (name, i, j)
+    return out
+
+
+@pytest.mark.parametrize("name", ["c256", "c512", "ml"])
+def test_full_size_cussen_sampled(name):
+    _full_size(name, P.CUSSEN, 40)
+
+
+def test_full_size_c256_schoolbook_sampled():
+    _full_size("c256", P.SCHOOLBOOK, 16)
