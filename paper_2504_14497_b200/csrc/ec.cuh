@@ -26,35 +26,49 @@ PCMM_HD void pt_identity(pt &r) {
 
 PCMM_HD bool pt_is_identity(const pt &a) { return fe_is_zero(a.Z); }
 
+// multiplication policies for the group law: inlined, or (device, hot loop) an
+// out-of-line call that keeps the loop body inside the instruction cache
+struct MulInline {
+    static PCMM_HD void mul(fe &r, const fe &a, const fe &b) { fe_mul(r, a, b); }
+};
+#if defined(__CUDA_ARCH__) && defined(PCMM_HAVE_FAST_MUL)
+struct MulCall {
+    static __device__ __forceinline__ void mul(fe &r, const fe &a, const fe &b) { r = fe_mul_call(a, b); }
+};
+#else
+typedef MulInline MulCall;
+#endif
+
 // RCB16 Algorithm 4: complete projective addition for a = -3.
-PCMM_HD void pt_add(pt &R, const pt &P, const pt &Q) {
+template <class M>
+PCMM_HD void pt_add_g(pt &R, const pt &P, const pt &Q) {
     fe t0, t1, t2, t3, t4, X3, Y3, Z3, b;
     fe_b_mont(b);
-    fe_mul(t0, P.X, Q.X);
-    fe_mul(t1, P.Y, Q.Y);
-    fe_mul(t2, P.Z, Q.Z);
+    M::mul(t0, P.X, Q.X);
+    M::mul(t1, P.Y, Q.Y);
+    M::mul(t2, P.Z, Q.Z);
     fe_add(t3, P.X, P.Y);
     fe_add(t4, Q.X, Q.Y);
-    fe_mul(t3, t3, t4);
+    M::mul(t3, t3, t4);
     fe_add(t4, t0, t1);
     fe_sub(t3, t3, t4);
     fe_add(t4, P.Y, P.Z);
     fe_add(X3, Q.Y, Q.Z);
-    fe_mul(t4, t4, X3);
+    M::mul(t4, t4, X3);
     fe_add(X3, t1, t2);
     fe_sub(t4, t4, X3);
     fe_add(X3, P.X, P.Z);
     fe_add(Y3, Q.X, Q.Z);
-    fe_mul(X3, X3, Y3);
+    M::mul(X3, X3, Y3);
     fe_add(Y3, t0, t2);
     fe_sub(Y3, X3, Y3);
-    fe_mul(Z3, b, t2);
+    M::mul(Z3, b, t2);
     fe_sub(X3, Y3, Z3);
     fe_add(Z3, X3, X3);
     fe_add(X3, X3, Z3);
     fe_sub(Z3, t1, X3);
     fe_add(X3, t1, X3);
-    fe_mul(Y3, b, Y3);
+    M::mul(Y3, b, Y3);
     fe_add(t1, t2, t2);
     fe_add(t2, t1, t2);
     fe_sub(Y3, Y3, t2);
@@ -64,19 +78,21 @@ PCMM_HD void pt_add(pt &R, const pt &P, const pt &Q) {
     fe_add(t1, t0, t0);
     fe_add(t0, t1, t0);
     fe_sub(t0, t0, t2);
-    fe_mul(t1, t4, Y3);
-    fe_mul(t2, t0, Y3);
-    fe_mul(Y3, X3, Z3);
+    M::mul(t1, t4, Y3);
+    M::mul(t2, t0, Y3);
+    M::mul(Y3, X3, Z3);
     fe_add(Y3, Y3, t2);
-    fe_mul(X3, t3, X3);
+    M::mul(X3, t3, X3);
     fe_sub(X3, X3, t1);
-    fe_mul(Z3, t4, Z3);
-    fe_mul(t1, t3, t0);
+    M::mul(Z3, t4, Z3);
+    M::mul(t1, t3, t0);
     fe_add(Z3, Z3, t1);
     R.X = X3;
     R.Y = Y3;
     R.Z = Z3;
 }
+
+PCMM_HD void pt_add(pt &R, const pt &P, const pt &Q) { pt_add_g<MulInline>(R, P, Q); }
 
 // RCB16 Algorithm 6: complete projective doubling for a = -3.
 PCMM_HD void pt_dbl(pt &R, const pt &P) {

@@ -101,7 +101,7 @@ PCMM_HD void fe_cond_sub_p(fe &r, const fe &a, uint32_t hi) {
 }
 
 // r = a + b mod p, a, b in [0, p)
-PCMM_HD void fe_add(fe &r, const fe &a, const fe &b) {
+PCMM_HD void fe_add_portable(fe &r, const fe &a, const fe &b) {
     fe s;
     uint64_t c = 0;
 #pragma unroll
@@ -114,7 +114,7 @@ PCMM_HD void fe_add(fe &r, const fe &a, const fe &b) {
 }
 
 // r = a - b mod p, a, b in [0, p)
-PCMM_HD void fe_sub(fe &r, const fe &a, const fe &b) {
+PCMM_HD void fe_sub_portable(fe &r, const fe &a, const fe &b) {
     uint32_t d[8];
     uint64_t borrow = 0;
 #pragma unroll
@@ -131,12 +131,6 @@ PCMM_HD void fe_sub(fe &r, const fe &a, const fe &b) {
         r.v[i] = (uint32_t)c;
         c >>= 32;
     }
-}
-
-PCMM_HD void fe_neg(fe &r, const fe &a) {
-    fe z;
-    fe_zero(z);
-    fe_sub(r, z, a);
 }
 
 // Montgomery multiplication r = a * b * 2^-256 mod p (portable reference form).
@@ -193,6 +187,28 @@ PCMM_HD void fe_mul(fe &r, const fe &a, const fe &b) {
 #else
     fe_mul_portable(r, a, b);
 #endif
+}
+
+PCMM_HD void fe_add(fe &r, const fe &a, const fe &b) {
+#if defined(__CUDA_ARCH__) && defined(PCMM_HAVE_FAST_MUL)
+    fe_add_fast(r, a, b);
+#else
+    fe_add_portable(r, a, b);
+#endif
+}
+
+PCMM_HD void fe_sub(fe &r, const fe &a, const fe &b) {
+#if defined(__CUDA_ARCH__) && defined(PCMM_HAVE_FAST_MUL)
+    fe_sub_fast(r, a, b);
+#else
+    fe_sub_portable(r, a, b);
+#endif
+}
+
+PCMM_HD void fe_neg(fe &r, const fe &a) {
+    fe z;
+    fe_zero(z);
+    fe_sub(r, z, a);
 }
 
 PCMM_HD void fe_sqr(fe &r, const fe &a) { fe_mul(r, a, a); }

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(ROWS) k_accum(const uint32_t *__restrict__ tab
                     Q.Y.v[q] = T[(1 * 8 + q) * kSlots];
                     Q.Z.v[q] = T[(2 * 8 + q) * kSlots];
                 }
-                pt_add(acc, acc, Q);
+                pt_add_g<MulCall>(acc, acc, Q);
             }
         }
     }
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__res
 #pragma unroll
         for (int c = 0; c < 4; c++) {
             if (VARIANT == 1) fe_mul_portable(x[c], x[c], y);
+            else if (VARIANT == 2) fe_add(x[c], x[c], y);
             else fe_mul(x[c], x[c], y);
         }
     }
@@ -106,6 +107,7 @@ cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int
 
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s) {
     if (variant == 1) k_bench_fp_mul<1><<<blocks, threads, 0, s>>>(iters, out);
+    else if (variant == 2) k_bench_fp_mul<2><<<blocks, threads, 0, s>>>(iters, out);
     else k_bench_fp_mul<0><<<blocks, threads, 0, s>>>(iters, out);
     return cudaGetLastError();
 }
