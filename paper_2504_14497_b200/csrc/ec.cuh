@@ -95,27 +95,28 @@ PCMM_HD void pt_add_g(pt &R, const pt &P, const pt &Q) {
 PCMM_HD void pt_add(pt &R, const pt &P, const pt &Q) { pt_add_g<MulInline>(R, P, Q); }
 
 // RCB16 Algorithm 6: complete projective doubling for a = -3.
-PCMM_HD void pt_dbl(pt &R, const pt &P) {
+template <class M>
+PCMM_HD void pt_dbl_g(pt &R, const pt &P) {
     fe t0, t1, t2, t3, X3, Y3, Z3, b;
     fe_b_mont(b);
-    fe_sqr(t0, P.X);
-    fe_sqr(t1, P.Y);
-    fe_sqr(t2, P.Z);
-    fe_mul(t3, P.X, P.Y);
+    M::mul(t0, P.X, P.X);
+    M::mul(t1, P.Y, P.Y);
+    M::mul(t2, P.Z, P.Z);
+    M::mul(t3, P.X, P.Y);
     fe_add(t3, t3, t3);
-    fe_mul(Z3, P.X, P.Z);
+    M::mul(Z3, P.X, P.Z);
     fe_add(Z3, Z3, Z3);
-    fe_mul(Y3, b, t2);
+    M::mul(Y3, b, t2);
     fe_sub(Y3, Y3, Z3);
     fe_add(X3, Y3, Y3);
     fe_add(Y3, X3, Y3);
     fe_sub(X3, t1, Y3);
     fe_add(Y3, t1, Y3);
-    fe_mul(Y3, X3, Y3);
-    fe_mul(X3, X3, t3);
+    M::mul(Y3, X3, Y3);
+    M::mul(X3, X3, t3);
     fe_add(t3, t2, t2);
     fe_add(t2, t2, t3);
-    fe_mul(Z3, b, Z3);
+    M::mul(Z3, b, Z3);
     fe_sub(Z3, Z3, t2);
     fe_sub(Z3, Z3, t0);
     fe_add(t3, Z3, Z3);
@@ -123,19 +124,21 @@ PCMM_HD void pt_dbl(pt &R, const pt &P) {
     fe_add(t3, t0, t0);
     fe_add(t0, t3, t0);
     fe_sub(t0, t0, t2);
-    fe_mul(t0, t0, Z3);
+    M::mul(t0, t0, Z3);
     fe_add(Y3, Y3, t0);
-    fe_mul(t0, P.Y, P.Z);
+    M::mul(t0, P.Y, P.Z);
     fe_add(t0, t0, t0);
-    fe_mul(Z3, t0, Z3);
+    M::mul(Z3, t0, Z3);
     fe_sub(X3, X3, Z3);
-    fe_mul(Z3, t0, t1);
+    M::mul(Z3, t0, t1);
     fe_add(Z3, Z3, Z3);
     fe_add(Z3, Z3, Z3);
     R.X = X3;
     R.Y = Y3;
     R.Z = Z3;
 }
+
+PCMM_HD void pt_dbl(pt &R, const pt &P) { pt_dbl_g<MulInline>(R, P); }
 
 // Out-of-line copies for the cold paths (table build, schoolbook ECSMs, encrypt,
 // decrypt): keeps compile time and code size bounded; the hot accumulate loop
@@ -149,9 +152,27 @@ PCMM_HD void pt_neg(pt &R, const pt &P) {
     R.Z = P.Z;
 }
 
-// v * P for a small signed integer v (|v| < 2^15): left-to-right binary
+// v * P for a small signed integer v (|v| < 2^31): left-to-right binary
 // double-and-add over the bits of |v|, then negation for v < 0 (R10:
 // -(|v| P) is the group element (q - |v|) P).  v = 0 gives the identity.
+template <class M>
+PCMM_HD void pt_mul_small_g(pt &R, int v, const pt &P) {
+    unsigned a = v < 0 ? (unsigned)(-v) : (unsigned)v;
+    pt acc;
+    pt_identity(acc);
+    int top = 31;
+    while (top >= 0 && !((a >> top) & 1u)) top--;
+    for (int i = top; i >= 0; i--) {
+        if (i != top) pt_dbl_g<M>(acc, acc);
+        if ((a >> i) & 1u) {
+            if (i == top) acc = P;
+            else pt_add_g<M>(acc, acc, P);
+        }
+    }
+    if (v < 0) pt_neg(acc, acc);
+    R = acc;
+}
+
 PCMM_HD void pt_mul_small(pt &R, int v, const pt &P) {
     unsigned a = v < 0 ? (unsigned)(-v) : (unsigned)v;
     pt acc;

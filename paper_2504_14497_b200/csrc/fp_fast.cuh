@@ -12,10 +12,9 @@
 //    a_i*b_j + T[i+j] never overflows, so each IMAD.WIDE also absorbs the
 //    running column word; the row's high words are then added with one carry
 //    chain (8 ALU ops per row, 64 IMAD.WIDE total);
-//  * reduction: P-256 Montgomery with -p^-1 mod 2^32 = 1 (q = T[i]); round i
-//    adds q at i+3 and i+6 and q*(2^32-1) at i+7..i+8 (the -q at limb i cancels
-//    it exactly).  The carry out of each round's 6-limb chain is deferred into the
-//    next round's top word (hi + E < 2^32 always), so no chain runs to the top;
+//  * reduction: P-256 Montgomery with 64-bit quotient digits (-p^-1 = 1 mod
+//    2^64): 4 rounds, each one 7-word carry chain; carries deferred between
+//    rounds (see below);
 //  * final conditional subtraction of p with a LOP3 select.
 #pragma once
 
@@ -68,28 +67,41 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
             : "r"(l[1]), "r"(h[0]), "r"(l[2]), "r"(h[1]), "r"(l[3]), "r"(h[2]), "r"(l[4]), "r"(h[3]), "r"(l[5]),
               "r"(h[4]), "r"(l[6]), "r"(h[5]), "r"(l[7]), "r"(h[6]), "r"(h[7]));
     }
-    // ---- reduction
+    // ---- reduction, 64-bit quotient digits: -p^-1 = 1 mod 2^64 (p = -1 mod 2^96),
+    // so round r (base b = 2r) takes q = T[b] + 2^32 T[b+1] and adds
+    //   q p 2^(32b) = -q + q 2^96 + u 2^192,  u = q (2^64 - 2^32 + 1) < 2^128.
+    // The -q cancels T[b], T[b+1] exactly; q 2^96 and u 2^192 go to words
+    // b+3..b+4 and b+6..b+9 in one carry chain.  The chain's carry out (word
+    // b+10) is deferred into the next round's u (word 2 of u' is word b+10;
+    // u' + 2^64 < 2^128), so no chain runs to the top.
     uint32_t E = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        const uint32_t q = T[i];
-        uint32_t lo, hh;
-        // (hh, lo) = q * (2^32 - 1) + E * 2^32  (hh = q - (q != 0) + E <= 2^32 - 1)
-        asm("sub.cc.u32 %0, 0, %2;\n\t"
-            "subc.u32 %1, %2, 0;"
-            : "=r"(lo), "=r"(hh)
-            : "r"(q));
-        hh += E;
-        asm("add.cc.u32 %0, %0, %7;\n\t"
-            "addc.cc.u32 %1, %1, 0;\n\t"
+    for (int r = 0; r < 4; r++) {
+        const int b = 2 * r;
+        const uint32_t q0 = T[b], q1 = T[b + 1];
+        uint32_t w1, w2, w3;
+        asm("sub.cc.u32 %0, %3, %4;\n\t"
+            "subc.cc.u32 %1, %4, %3;\n\t"
+            "subc.u32 %2, %3, 0;"
+            : "=r"(w1), "=r"(w2), "=r"(w3)
+            : "r"(q1), "r"(q0));
+        if (r > 0) {
+            asm("add.cc.u32 %0, %0, %2;\n\t"
+                "addc.u32 %1, %1, 0;"
+                : "+r"(w2), "+r"(w3)
+                : "r"(E));
+        }
+        asm("add.cc.u32 %0, %0, %8;\n\t"
+            "addc.cc.u32 %1, %1, %9;\n\t"
             "addc.cc.u32 %2, %2, 0;\n\t"
-            "addc.cc.u32 %3, %3, %7;\n\t"
-            "addc.cc.u32 %4, %4, %8;\n\t"
-            "addc.cc.u32 %5, %5, %9;\n\t"
-            "addc.u32 %6, 0, 0;"
-            : "+r"(T[i + 3]), "+r"(T[i + 4]), "+r"(T[i + 5]), "+r"(T[i + 6]), "+r"(T[i + 7]), "+r"(T[i + 8]),
-              "=r"(E)
-            : "r"(q), "r"(lo), "r"(hh));
+            "addc.cc.u32 %3, %3, %8;\n\t"
+            "addc.cc.u32 %4, %4, %10;\n\t"
+            "addc.cc.u32 %5, %5, %11;\n\t"
+            "addc.cc.u32 %6, %6, %12;\n\t"
+            "addc.u32 %7, 0, 0;"
+            : "+r"(T[b + 3]), "+r"(T[b + 4]), "+r"(T[b + 5]), "+r"(T[b + 6]), "+r"(T[b + 7]), "+r"(T[b + 8]),
+              "+r"(T[b + 9]), "=r"(E)
+            : "r"(q0), "r"(q1), "r"(w1), "r"(w2), "r"(w3));
     }
     // ---- result = E*2^256 + T[8..15] < 2p; subtract p if it is >= p
     uint32_t t[8], m;

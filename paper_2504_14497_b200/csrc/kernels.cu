@@ -221,9 +221,22 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
 // ------------------------------------------------------------ a2 + a3: tables
 // Thread per (component c, column k, output column j); j fastest so that the
 // loads of Enc(b_kj) are coalesced.  Reconstruction (Alg. 2 lines 14-23) in the
-// recursive form b^(w)[u] = b^(w)[u-1] + b^(w+1)[ptr^(w)[u]] (R3, R7).
-__global__ void k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans, int n, int l, int N,
-                         uint32_t *__restrict__ tables) {
+// recursive form b^(w)[u] = b^(w)[u-1] + b^(w+1)[ptr^(w)[u]] (R3, R7): levels
+// >= 2 (at most 8 entries for w <= 4) live in a small local array; level 1 is
+// produced as a running prefix sum and written straight to the table.
+constexpr int kMaxUpper = 8;
+
+__device__ __forceinline__ void table_store(uint32_t *dst, int slot, const pt &q) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        dst[(0 * 8 + i) * kSlots + slot] = q.X.v[i];
+        dst[(1 * 8 + i) * kSlots + slot] = q.Y.v[i];
+        dst[(2 * 8 + i) * kSlots + slot] = q.Z.v[i];
+    }
+}
+
+__global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
+                                                int n, int l, int N, uint32_t *__restrict__ tables) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -234,31 +247,39 @@ __global__ void k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__res
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     const ColPlan pl = plans[k];
-    pt cur[kMaxVals], nxt[kMaxVals];
-    int ncur = pl.n[N - 1];
-    for (int u = 0; u < ncur; u++) pt_mul_small(cur[u], pl.sN[u], P);     // Alg. 3 line 5
-    for (int lev = N - 1; lev >= 1; lev--) {
-        int nl = pl.n[lev - 1];
-        for (int u = 0; u < nl; u++) {
-            const pt &g = cur[pl.ptr[lev - 1][u]];
-            if (u == 0) nxt[0] = g;
-            else pt_add_nl(nxt[u], nxt[u - 1], g);                          // prefix sum
-        }
-        for (int u = 0; u < nl; u++) cur[u] = nxt[u];
-        ncur = nl;
-    }
     uint32_t *dst = tables + (((int64_t)c * n + k) * l + j) * kTableWords;
     pt id;
     pt_identity(id);
-    for (int slot = 0; slot < kSlots; slot++) {
-        const pt &q = (slot >= 1 && slot <= ncur) ? cur[slot - 1] : id;
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            dst[(0 * 8 + i) * kSlots + slot] = q.X.v[i];
-            dst[(1 * 8 + i) * kSlots + slot] = q.Y.v[i];
-            dst[(2 * 8 + i) * kSlots + slot] = q.Z.v[i];
+    table_store(dst, 0, id);
+    const int n1 = pl.n[0];
+    if (N == 1) {
+        for (int u = 0; u < n1; u++) {                                      // Alg. 3 line 5 only
+            pt e;
+            pt_mul_small_g<MulCall>(e, pl.sN[u], P);
+            table_store(dst, u + 1, e);
+        }
+    } else {
+        pt up[kMaxUpper];                                                   // level w+1 entries
+        int nup = pl.n[N - 1];
+        for (int u = 0; u < nup; u++) pt_mul_small_g<MulCall>(up[u], pl.sN[u], P);   // line 5
+        for (int lev = N - 1; lev >= 2; lev--) {
+            pt cur[kMaxUpper];
+            const int nl = pl.n[lev - 1];
+            for (int u = 0; u < nl; u++) {
+                const pt &g = up[pl.ptr[lev - 1][u]];
+                if (u == 0) cur[0] = g;
+                else pt_add_g<MulCall>(cur[u], cur[u - 1], g);               // prefix sum
+            }
+            for (int u = 0; u < nl; u++) up[u] = cur[u];
+        }
+        pt run = up[pl.ptr[0][0]];
+        table_store(dst, 1, run);
+        for (int u = 1; u < n1; u++) {
+            pt_add_g<MulCall>(run, run, up[pl.ptr[0][u]]);                   // level-1 prefix sum
+            table_store(dst, u + 1, run);
         }
     }
+    for (int slot = n1 + 1; slot < kSlots; slot++) table_store(dst, slot, id);
 }
 
 // ------------------------------------------------------------ a5: split-k reduce
@@ -546,7 +567,7 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
 
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, uint32_t *tables,
                           cudaStream_t s) {
-    k_tables<<<blocks_for(2LL * n * l, 64), 64, 0, s>>>(bsoa, plans, n, l, N, tables);
+    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, tables);
     return cudaGetLastError();
 }
 

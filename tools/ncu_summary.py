@@ -1,0 +1,29 @@
+"""Summarise an ncu --set full report (run here, no GPU): occupancy, issue, pipes, stalls, DRAM."""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units, vals = rows[0], rows[1], rows[2]
+d = dict(zip(hdr, vals))
+u = dict(zip(hdr, units))
+keys = ["Kernel Name", "gpu__time_duration.sum", "launch__registers_per_thread", "launch__occupancy_limit_registers",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+        "sm__cycles_elapsed.avg.per_second"]
+for k in keys:
+    if k in d:
+        print(f"{k:75s} {d[k]:>18s} {u.get(k, '')}")
+stalls = [(k, float(v.replace(",", ""))) for k, v in d.items()
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued") and v]
+tot = sum(v for _, v in stalls) or 1
+print("--- pc-sampling stall reasons (share of samples)")
+for k, v in sorted(stalls, key=lambda x: -x[1])[:10]:
+    print(f"  {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):30s} {100 * v / tot:6.1f}%")
