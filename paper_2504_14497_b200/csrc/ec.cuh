@@ -39,6 +39,69 @@ struct MulCall {
 typedef MulInline MulCall;
 #endif
 
+#if defined(__CUDA_ARCH__) && defined(PCMM_HAVE_FAST_MUL)
+// RCB16 Algorithm 4 with its 14 products grouped into 7 independent pairs
+// (same operations as pt_add_g, reordered along the data flow; each pair is one
+// out-of-line call that interleaves two Montgomery products).
+__device__ __forceinline__ void mul2(fe &r0, const fe &a0, const fe &b0, fe &r1, const fe &a1, const fe &b1) {
+    fe2 r = fe_mul2_call(a0, b0, a1, b1);
+    r0 = r.x;
+    r1 = r.y;
+}
+
+__device__ __forceinline__ void pt_add_pair(pt &R, const pt &P, const pt &Q) {
+    fe m1, m2, m3, m4, m5, m6, s0, s1, b;
+    fe_b_mont(b);
+    mul2(m1, P.X, Q.X, m2, P.Y, Q.Y);              // t0 = X1 X2, t1 = Y1 Y2
+    fe_add(s0, P.X, P.Y);
+    fe_add(s1, Q.X, Q.Y);
+    mul2(m3, P.Z, Q.Z, m4, s0, s1);                // t2 = Z1 Z2, t3 = (X1+Y1)(X2+Y2)
+    fe_add(s0, P.Y, P.Z);
+    fe_add(s1, Q.Y, Q.Z);
+    fe a0, a1;
+    fe_add(a0, P.X, P.Z);
+    fe_add(a1, Q.X, Q.Z);
+    mul2(m5, s0, s1, m6, a0, a1);                  // t4 = (Y1+Z1)(Y2+Z2), X3 = (X1+Z1)(X2+Z2)
+    fe t3, t4, y3;
+    fe_add(s0, m1, m2);
+    fe_sub(t3, m4, s0);                            // t3 = t3 - (t0 + t1)
+    fe_add(s0, m2, m3);
+    fe_sub(t4, m5, s0);                            // t4 = t4 - (t1 + t2)
+    fe_add(s0, m1, m3);
+    fe_sub(y3, m6, s0);                            // Y3 = X3 - (t0 + t2)
+    fe m7, m8;
+    mul2(m7, b, m3, m8, b, y3);                    // Z3 = b t2, Y3 = b Y3
+    fe x3, z3;
+    fe_sub(x3, y3, m7);                            // X3 = Y3 - Z3
+    fe_add(z3, x3, x3);
+    fe_add(x3, x3, z3);                            // X3 = 3 X3
+    fe_sub(z3, m2, x3);                            // Z3 = t1 - X3
+    fe_add(x3, m2, x3);                            // X3 = t1 + X3
+    fe t2b;
+    fe_add(s0, m3, m3);
+    fe_add(t2b, s0, m3);                           // t2 = 3 t2
+    fe_sub(y3, m8, t2b);
+    fe_sub(y3, y3, m1);                            // Y3 = Y3 - t2 - t0
+    fe_add(s0, y3, y3);
+    fe_add(y3, s0, y3);                            // Y3 = 3 Y3
+    fe t0b;
+    fe_add(s0, m1, m1);
+    fe_add(t0b, s0, m1);
+    fe_sub(t0b, t0b, t2b);                         // t0 = 3 t0 - t2
+    fe m9, m10, m11, m12, m13, m14;
+    mul2(m9, t4, y3, m10, t0b, y3);                // t1 = t4 Y3, t2 = t0 Y3
+    mul2(m11, x3, z3, m12, t3, x3);                // Y3 = X3 Z3, X3 = t3 X3
+    mul2(m13, t4, z3, m14, t3, t0b);               // Z3 = t4 Z3, t1 = t3 t0
+    fe_add(R.Y, m11, m10);
+    fe_sub(R.X, m12, m9);
+    fe_add(R.Z, m13, m14);
+}
+#else
+template <class M> PCMM_HD void pt_add_g(pt &R, const pt &P, const pt &Q);
+struct MulInline;
+PCMM_HD void pt_add_pair(pt &R, const pt &P, const pt &Q) { pt_add_g<MulInline>(R, P, Q); }
+#endif
+
 // RCB16 Algorithm 4: complete projective addition for a = -3.
 template <class M>
 PCMM_HD void pt_add_g(pt &R, const pt &P, const pt &Q) {

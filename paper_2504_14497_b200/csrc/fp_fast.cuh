@@ -194,4 +194,17 @@ __device__ __noinline__ fe fe_mul_call(const fe a, const fe b) {
     return r;
 }
 
+struct fe2 {
+    fe x, y;
+};
+
+// Two independent Montgomery products in one out-of-line call: ptxas
+// interleaves the two dependency chains (twice the ILP of a single call).
+__device__ __noinline__ fe2 fe_mul2_call(const fe a0, const fe b0, const fe a1, const fe b1) {
+    fe2 r;
+    fe_mul_fast(r.x, a0, b0);
+    fe_mul_fast(r.y, a1, b1);
+    return r;
+}
+
 }  // namespace pcmm

@@ -1,6 +1,8 @@
 // hot.cu -- the dominant kernel of the Cussen path (step a4 of SURVEY.md §8(a))
 // and the fp_mul throughput probe, in their own translation unit (parallel
 // compilation; the hot loop inlines the complete addition and fe_mul).
+#include <stdlib.h>
+
 #include "ec.cuh"
 #include "internal.h"
 
@@ -20,8 +22,8 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 // Per k-chunk the CTA stages KCH tables (1536 B each, [coord][limb][slot]) in
 // shared memory; a warp reads, for one k, at most 15 distinct words per
 // (coord, limb) within 16 consecutive banks: conflict-free gathers.
-template <int ROWS, int KCH>
-__global__ void __launch_bounds__(ROWS) k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
+template <int ROWS, int KCH, int MINB>
+__global__ void __launch_bounds__(ROWS, MINB) k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
                                                 int m, int n, int l, int ksplit, uint32_t *__restrict__ out,
                                                 int64_t split_stride) {
     extern __shared__ uint4 smem4[];
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(ROWS) k_accum(const uint32_t *__restrict__ tab
                     Q.Y.v[q] = T[(1 * 8 + q) * kSlots];
                     Q.Z.v[q] = T[(2 * 8 + q) * kSlots];
                 }
-                pt_add_g<MulCall>(acc, acc, Q);
+                pt_add_pair(acc, acc, Q);
             }
         }
     }
@@ -98,10 +100,21 @@ cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int
     const int rowblocks = (m + kRows - 1) / kRows;
     const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
     const size_t smem = (size_t)kChunk * kTableWords * 4;
-    cudaError_t err = cudaFuncSetAttribute(k_accum<kRows, kChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-    if (err) return err;
-    k_accum<kRows, kChunk><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);
+    static int minb = -1;
+    if (minb < 0) {
+        const char *e = getenv("PCMM_ACCUM_MINB");
+        minb = e ? atoi(e) : 3;
+    }
+    cudaError_t err;
+    if (minb == 4) {
+        err = cudaFuncSetAttribute(k_accum<kRows, kChunk, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err) return err;
+        k_accum<kRows, kChunk, 4><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);
+    } else {
+        err = cudaFuncSetAttribute(k_accum<kRows, kChunk, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err) return err;
+        k_accum<kRows, kChunk, 3><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);
+    }
     return cudaGetLastError();
 }
 
