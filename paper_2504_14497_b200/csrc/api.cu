@@ -7,6 +7,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -64,13 +65,20 @@ Layout layout(int m, int n, int l, int path) {
     L.bsoa = off;
     off = align256(off + cnt * 2 * kPtWords * 4);
     if (path == PCMM_PATH_CUSSEN) {
-        L.rows = 128;                      // k_accum CTA = 128 rows (hot.cu kRows)
+        L.rows = accum_rows();
         const int rowblocks = (m + L.rows - 1) / L.rows;
         const int64_t base = (int64_t)l * 2 * rowblocks;
-        const int64_t target = 8LL * num_sms();            // enough CTAs to fill the chip
-        int ks = (int)((target + base - 1) / base);
-        if (ks > n) ks = n;
-        if (ks < 1) ks = 1;
+        // split-k factor: minimise the quantised wave count per unit of work,
+        // ceil(base*ks / resident) / ks, plus a small charge per extra split
+        // (the k_reduce additions and per-CTA chunk overheads).
+        const double resident = (double)num_sms() * accum_ctas_per_sm();
+        int ks = 1;
+        double best = 1e30;
+        for (int cand = 1; cand <= 16 && cand <= n; cand++) {
+            const double waves = std::ceil((double)base * cand / resident);
+            const double cost = waves / cand * (1.0 + 0.01 * (cand - 1)) + (n / cand < 8 ? 1.0 : 0.0);
+            if (cost < best - 1e-9) { best = cost; ks = cand; }
+        }
         L.ksplit = ks;
         L.plans = off;
         off = align256(off + (size_t)n * sizeof(ColPlan));

@@ -94,19 +94,43 @@ __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__res
 constexpr int kChunk = 32;
 constexpr int kRows = 128;
 
+static int accum_minb() {
+    static int minb = -1;
+    if (minb < 0) {
+        const char *e = getenv("PCMM_ACCUM_MINB");
+        minb = e ? atoi(e) : 3;
+    }
+    return minb;
+}
+
+// resident k_accum CTAs per SM (for wave-balanced split-k choice)
+int accum_ctas_per_sm() {
+    static int occ = 0;
+    if (!occ) {
+        const size_t smem = (size_t)kChunk * kTableWords * 4;
+        cudaError_t e;
+        if (accum_minb() == 4) {
+            cudaFuncSetAttribute(k_accum<kRows, kChunk, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<kRows, kChunk, 4>, kRows, smem);
+        } else {
+            cudaFuncSetAttribute(k_accum<kRows, kChunk, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<kRows, kChunk, 3>, kRows, smem);
+        }
+        if (e != cudaSuccess || occ <= 0) occ = 3;
+    }
+    return occ;
+}
+
+int accum_rows() { return kRows; }
+
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int rows, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
     (void)rows;
     const int rowblocks = (m + kRows - 1) / kRows;
     const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
     const size_t smem = (size_t)kChunk * kTableWords * 4;
-    static int minb = -1;
-    if (minb < 0) {
-        const char *e = getenv("PCMM_ACCUM_MINB");
-        minb = e ? atoi(e) : 3;
-    }
     cudaError_t err;
-    if (minb == 4) {
+    if (accum_minb() == 4) {
         err = cudaFuncSetAttribute(k_accum<kRows, kChunk, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err) return err;
         k_accum<kRows, kChunk, 4><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);

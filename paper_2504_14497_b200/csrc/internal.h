@@ -62,5 +62,7 @@ cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const 
                               int64_t count, cudaStream_t s);
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s);
 int num_sms();
+int accum_ctas_per_sm();
+int accum_rows();
 
 }  // namespace pcmm

@@ -268,14 +268,14 @@ __global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bso
             for (int u = 0; u < nl; u++) {
                 const pt &g = up[pl.ptr[lev - 1][u]];
                 if (u == 0) cur[0] = g;
-                else pt_add_g<MulCall>(cur[u], cur[u - 1], g);               // prefix sum
+                else pt_add_pair(cur[u], cur[u - 1], g);                        // prefix sum
             }
             for (int u = 0; u < nl; u++) up[u] = cur[u];
         }
         pt run = up[pl.ptr[0][0]];
         table_store(dst, 1, run);
         for (int u = 1; u < n1; u++) {
-            pt_add_g<MulCall>(run, run, up[pl.ptr[0][u]]);                   // level-1 prefix sum
+            pt_add_pair(run, run, up[pl.ptr[0][u]]);                        // level-1 prefix sum
             table_store(dst, u + 1, run);
         }
     }
