@@ -55,10 +55,10 @@ std::vector<ProfRec> g_prof;
 // ---------------------------------------------------------------- workspace
 struct Layout {
     size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, partial = 0, total = 0;
-    int rows = 128, ksplit = 1;
+    int rows = 128, ksplit = 1, slots = 16;
 };
 
-Layout layout(int m, int n, int l, int path) {
+Layout layout(int m, int n, int l, int w, int path) {
     Layout L;
     size_t off = 256;                      // status word(s)
     const size_t cnt = (size_t)n * l;
@@ -71,7 +71,8 @@ Layout layout(int m, int n, int l, int path) {
         // split-k factor: minimise the quantised wave count per unit of work,
         // ceil(base*ks / resident) / ks, plus a small charge per extra split
         // (the k_reduce additions and per-CTA chunk overheads).
-        const double resident = (double)num_sms() * accum_ctas_per_sm();
+        L.slots = table_slots(w);
+        const double resident = (double)num_sms() * accum_ctas_per_sm(L.slots);
         int ks = 1;
         double best = 1e30;
         for (int cand = 1; cand <= 16 && cand <= n; cand++) {
@@ -85,7 +86,7 @@ Layout layout(int m, int n, int l, int path) {
         L.rank = off;
         off = align256(off + (size_t)n * m);
         L.tables = off;
-        off = align256(off + cnt * 2 * kTableWords * 4);
+        off = align256(off + cnt * 2 * (size_t)kPtWords * L.slots * 4);
         if (ks > 1) {
             L.partial = off;
             off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
@@ -170,7 +171,7 @@ size_t pcmm_workspace_bytes(int m, int n, int l, int w, int path) {
     if (path == -1) return 256;
     if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 8) return 0;
     if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN) return 0;
-    return layout(m, n, l, path).total;
+    return layout(m, n, l, w, path).total;
 }
 
 int pcmm_keygen(uint64_t seed, uint8_t sk_h[32], uint8_t pk_h[64]) {
@@ -224,7 +225,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         if (w > 4) return fail(PCMM_ENOTSUP, "Cussen path supports w <= 4 in this build");
         if (iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "iters must be in [1, 4]");
     }
-    const Layout L = layout(m, n, l, path);
+    const Layout L = layout(m, n, l, w, path);
     if (ws_bytes < L.total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_workspace_bytes)");
     uint8_t *ws = (uint8_t *)ws_d;
     int *status = (int *)ws;
@@ -240,13 +241,13 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint8_t *rank = ws + L.rank;
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
-    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, tables, s));
+    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, tables, s));
     const int64_t cnt = (int64_t)m * l;
     if (L.ksplit == 1) {
-        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.rows, 1, out, 0, s));
+        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, 1, out, 0, s));
     } else {
         uint32_t *partial = (uint32_t *)(ws + L.partial);
-        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.rows, L.ksplit, partial, 2LL * kPtWords * cnt, s));
+        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, L.ksplit, partial, 2LL * kPtWords * cnt, s));
         LAUNCH("reduce", s, launch_reduce_splits(partial, L.ksplit, cnt, out, s));
     }
     return PCMM_OK;

@@ -1,8 +1,6 @@
 // hot.cu -- the dominant kernel of the Cussen path (step a4 of SURVEY.md §8(a))
 // and the fp_mul throughput probe, in their own translation unit (parallel
 // compilation; the hot loop inlines the complete addition and fe_mul).
-#include <stdlib.h>
-
 #include "ec.cuh"
 #include "internal.h"
 
@@ -19,45 +17,80 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 
 // ------------------------------------------------------------ a4: accumulate
 // CTA = (output column j, component c, row block, k-split).  Thread = row i.
-// Per k-chunk the CTA stages KCH tables (1536 B each, [coord][limb][slot]) in
-// shared memory; a warp reads, for one k, at most 15 distinct words per
-// (coord, limb) within 16 consecutive banks: conflict-free gathers.
-template <int ROWS, int KCH, int MINB>
-__global__ void __launch_bounds__(ROWS, MINB) k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
-                                                int m, int n, int l, int ksplit, uint32_t *__restrict__ out,
-                                                int64_t split_stride) {
+// Tables hold S = 2^w slots per (k, j, c) ([coord][limb][slot], slot 0 = the
+// identity), so a warp's gather for one k touches at most S consecutive banks
+// per (coord, limb): conflict-free.  Per chunk of KCH = min(128, 512/S) columns
+// the CTA stages the tables (48 KB) and the rank bytes of its rows in shared
+// memory; each lane then walks ITS OWN nonzero entries of the chunk (a_ik = 0
+// adds the identity and is skipped, R1), so a warp runs max-over-lanes
+// of the nonzero count instead of KCH additions (25% zeros at w = 2).
+template <int S>
+struct AccumCfg {
+    static constexpr int kRows = 128;
+    static constexpr int kChunk = (512 / S) < 128 ? (512 / S) : 128;
+    static constexpr int kTW = kPtWords * S;                       // words per table
+    static constexpr size_t kSmem = (size_t)kChunk * kTW * 4 + (size_t)kChunk * kRows;
+};
+
+template <int S>
+__global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
+    k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
+            uint32_t *__restrict__ out, int64_t split_stride) {
+    constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk, TW = AccumCfg<S>::kTW;
     extern __shared__ uint4 smem4[];
-    const uint32_t *smem = reinterpret_cast<const uint32_t *>(smem4);
+    const uint32_t *tsm = reinterpret_cast<const uint32_t *>(smem4);
+    uint8_t *rsm = reinterpret_cast<uint8_t *>(smem4) + (size_t)KCH * TW * 4;
     int b = blockIdx.x;
     const int j = b % l; b /= l;
     const int c = b & 1; b >>= 1;
     const int rowblocks = (m + ROWS - 1) / ROWS;
     const int rb = b % rowblocks;
     const int s = b / rowblocks;
-    const int i = rb * ROWS + (int)threadIdx.x;
+    const int tid = (int)threadIdx.x;
+    const int i = rb * ROWS + tid;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
     pt acc;
     pt_identity(acc);
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
-        for (int t = threadIdx.x; t < kc * (kTableWords / 4); t += ROWS) {
-            const int kk = t / (kTableWords / 4), wd = t % (kTableWords / 4);
-            const uint4 *src = reinterpret_cast<const uint4 *>(
-                tables + (((int64_t)c * n + (k0 + kk)) * l + j) * kTableWords);
-            smem4[kk * (kTableWords / 4) + wd] = src[wd];
+        for (int t = tid; t < kc * (TW / 4); t += ROWS) {
+            const int kk = t / (TW / 4), wd = t % (TW / 4);
+            const uint4 *src = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW);
+            smem4[kk * (TW / 4) + wd] = src[wd];
+        }
+        for (int t = tid; t < kc * ROWS; t += ROWS) {
+            const int row = rb * ROWS + (t % ROWS);
+            rsm[t] = row < m ? rank[(int64_t)(k0 + t / ROWS) * m + row] : (uint8_t)0;
         }
         __syncthreads();
-        if (i < m) {
-            for (int kk = 0; kk < kc; kk++) {
-                const int u = rank[(int64_t)(k0 + kk) * m + i];
-                const uint32_t *T = smem + kk * kTableWords + u;
+        if (S <= 4) {
+            // w <= 2: >= 25% zeros -- each lane walks its own nonzero entries
+            int kk = 0;
+            while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
+            while (kk < kc) {
+                const uint32_t *T = tsm + kk * TW + rsm[kk * ROWS + tid];
                 pt Q;
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                    Q.X.v[q] = T[(0 * 8 + q) * kSlots];
-                    Q.Y.v[q] = T[(1 * 8 + q) * kSlots];
-                    Q.Z.v[q] = T[(2 * 8 + q) * kSlots];
+                    Q.X.v[q] = T[(0 * 8 + q) * S];
+                    Q.Y.v[q] = T[(1 * 8 + q) * S];
+                    Q.Z.v[q] = T[(2 * 8 + q) * S];
+                }
+                pt_add_pair(acc, acc, Q);
+                kk++;
+                while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
+            }
+        } else {
+            // w >= 3: few zeros -- warp-uniform loop (a zero adds the identity in slot 0)
+            for (int kk = 0; kk < kc; kk++) {
+                const uint32_t *T = tsm + kk * TW + rsm[kk * ROWS + tid];
+                pt Q;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    Q.X.v[q] = T[(0 * 8 + q) * S];
+                    Q.Y.v[q] = T[(1 * 8 + q) * S];
+                    Q.Z.v[q] = T[(2 * 8 + q) * S];
                 }
                 pt_add_pair(acc, acc, Q);
             }
@@ -91,55 +124,54 @@ __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__res
     for (int i = 0; i < 8; i++) out[t * 8 + i] = x[0].v[i] ^ x[1].v[i] ^ x[2].v[i] ^ x[3].v[i];
 }
 
-constexpr int kChunk = 32;
-constexpr int kRows = 128;
-
-static int accum_minb() {
-    static int minb = -1;
-    if (minb < 0) {
-        const char *e = getenv("PCMM_ACCUM_MINB");
-        minb = e ? atoi(e) : 3;
-    }
-    return minb;
-}
-
-// resident k_accum CTAs per SM (for wave-balanced split-k choice)
-int accum_ctas_per_sm() {
-    static int occ = 0;
-    if (!occ) {
-        const size_t smem = (size_t)kChunk * kTableWords * 4;
-        cudaError_t e;
-        if (accum_minb() == 4) {
-            cudaFuncSetAttribute(k_accum<kRows, kChunk, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<kRows, kChunk, 4>, kRows, smem);
-        } else {
-            cudaFuncSetAttribute(k_accum<kRows, kChunk, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<kRows, kChunk, 3>, kRows, smem);
-        }
-        if (e != cudaSuccess || occ <= 0) occ = 3;
-    }
+template <int S>
+static int ctas_per_sm_s() {
+    int occ = 0;
+    cudaFuncSetAttribute(k_accum<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S>::kSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<S>, AccumCfg<S>::kRows, AccumCfg<S>::kSmem) !=
+            cudaSuccess ||
+        occ <= 0)
+        occ = 3;
     return occ;
 }
 
-int accum_rows() { return kRows; }
-
-cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int rows, int ksplit,
-                         uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
-    (void)rows;
-    const int rowblocks = (m + kRows - 1) / kRows;
-    const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
-    const size_t smem = (size_t)kChunk * kTableWords * 4;
-    cudaError_t err;
-    if (accum_minb() == 4) {
-        err = cudaFuncSetAttribute(k_accum<kRows, kChunk, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err) return err;
-        k_accum<kRows, kChunk, 4><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);
-    } else {
-        err = cudaFuncSetAttribute(k_accum<kRows, kChunk, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err) return err;
-        k_accum<kRows, kChunk, 3><<<grid, kRows, smem, s>>>(tables, rank, m, n, l, ksplit, out, out_stride_split);
+// resident k_accum CTAs per SM for table slot count S = 2^w (wave-balanced split-k)
+int accum_ctas_per_sm(int slots) {
+    static int occ[17] = {0};
+    if (slots < 2 || slots > 16) slots = 16;
+    if (!occ[slots]) {
+        switch (slots) {
+            case 2: occ[slots] = ctas_per_sm_s<2>(); break;
+            case 4: occ[slots] = ctas_per_sm_s<4>(); break;
+            case 8: occ[slots] = ctas_per_sm_s<8>(); break;
+            default: occ[slots] = ctas_per_sm_s<16>(); break;
+        }
     }
+    return occ[slots];
+}
+
+int accum_rows() { return AccumCfg<16>::kRows; }
+
+template <int S>
+static cudaError_t launch_accum_s(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int ksplit,
+                                  uint32_t *out, int64_t stride, cudaStream_t s) {
+    const int rowblocks = (m + AccumCfg<S>::kRows - 1) / AccumCfg<S>::kRows;
+    const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
+    cudaError_t err =
+        cudaFuncSetAttribute(k_accum<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S>::kSmem);
+    if (err) return err;
+    k_accum<S><<<grid, AccumCfg<S>::kRows, AccumCfg<S>::kSmem, s>>>(tables, rank, m, n, l, ksplit, out, stride);
     return cudaGetLastError();
+}
+
+cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
+                         uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+    switch (slots) {
+        case 2: return launch_accum_s<2>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        case 4: return launch_accum_s<4>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        case 8: return launch_accum_s<8>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        default: return launch_accum_s<16>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+    }
 }
 
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s) {

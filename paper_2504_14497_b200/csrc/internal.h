@@ -18,9 +18,9 @@ struct ColPlan {
 };
 
 constexpr int kMaxVals = 15;          // |a^(1)| <= 2^w - 1 for w <= 4 (signed: 15 nonzero values)
-constexpr int kSlots = 16;            // table slots per (k, j, c): slot 0 = infinity
 constexpr int kPtWords = 24;          // X, Y, Z x 8 limbs
-constexpr int kTableWords = kPtWords * kSlots;   // 384 words = 1536 B per (k, j, c)
+// table slots per (k, j, c) = 2^w (slot 0 = infinity, slots 1..|a^(1)| = entries)
+inline int table_slots(int w) { return 1 << (w < 1 ? 1 : w); }
 
 // status word bits (workspace offset 0)
 constexpr int kStatusBound = 1;
@@ -38,9 +38,9 @@ void prof_end(cudaStream_t s);
 cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *status, cudaStream_t s);
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s);
-cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, uint32_t *tables,
-                          cudaStream_t s);
-cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int rows, int ksplit,
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+                          uint32_t *tables, cudaStream_t s);
+cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s);
 cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);
 cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
@@ -62,7 +62,7 @@ cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const 
                               int64_t count, cudaStream_t s);
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s);
 int num_sms();
-int accum_ctas_per_sm();
+int accum_ctas_per_sm(int slots);
 int accum_rows();
 
 }  // namespace pcmm

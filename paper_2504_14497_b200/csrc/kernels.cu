@@ -226,17 +226,17 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
 // produced as a running prefix sum and written straight to the table.
 constexpr int kMaxUpper = 8;
 
-__device__ __forceinline__ void table_store(uint32_t *dst, int slot, const pt &q) {
+__device__ __forceinline__ void table_store(uint32_t *dst, int S, int slot, const pt &q) {
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        dst[(0 * 8 + i) * kSlots + slot] = q.X.v[i];
-        dst[(1 * 8 + i) * kSlots + slot] = q.Y.v[i];
-        dst[(2 * 8 + i) * kSlots + slot] = q.Z.v[i];
+        dst[(0 * 8 + i) * S + slot] = q.X.v[i];
+        dst[(1 * 8 + i) * S + slot] = q.Y.v[i];
+        dst[(2 * 8 + i) * S + slot] = q.Z.v[i];
     }
 }
 
 __global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
-                                                int n, int l, int N, uint32_t *__restrict__ tables) {
+                                                int n, int l, int N, int S, uint32_t *__restrict__ tables) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -247,16 +247,16 @@ __global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bso
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     const ColPlan pl = plans[k];
-    uint32_t *dst = tables + (((int64_t)c * n + k) * l + j) * kTableWords;
+    uint32_t *dst = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
     pt id;
     pt_identity(id);
-    table_store(dst, 0, id);
+    table_store(dst, S, 0, id);
     const int n1 = pl.n[0];
     if (N == 1) {
         for (int u = 0; u < n1; u++) {                                      // Alg. 3 line 5 only
             pt e;
             pt_mul_small_g<MulCall>(e, pl.sN[u], P);
-            table_store(dst, u + 1, e);
+            table_store(dst, S, u + 1, e);
         }
     } else {
         pt up[kMaxUpper];                                                   // level w+1 entries
@@ -273,13 +273,13 @@ __global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bso
             for (int u = 0; u < nl; u++) up[u] = cur[u];
         }
         pt run = up[pl.ptr[0][0]];
-        table_store(dst, 1, run);
+        table_store(dst, S, 1, run);
         for (int u = 1; u < n1; u++) {
             pt_add_pair(run, run, up[pl.ptr[0][u]]);                        // level-1 prefix sum
-            table_store(dst, u + 1, run);
+            table_store(dst, S, u + 1, run);
         }
     }
-    for (int slot = n1 + 1; slot < kSlots; slot++) table_store(dst, slot, id);
+    for (int slot = n1 + 1; slot < S; slot++) table_store(dst, S, slot, id);
 }
 
 // ------------------------------------------------------------ a5: split-k reduce
@@ -565,9 +565,9 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, uint32_t *tables,
-                          cudaStream_t s) {
-    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, tables);
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+                          uint32_t *tables, cudaStream_t s) {
+    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, tables);
     return cudaGetLastError();
 }
 
