@@ -50,6 +50,32 @@ def env_int(k, d):
         return d
 
 
+def workload_config(cfg, path: str, world: int) -> dict:
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": f"{cfg.name}: PC-MM {cfg.m}x{cfg.n} by {cfg.n}x{cfg.l}, w={cfg.w}"
+                        f"{' signed' if cfg.signed else ''}, B in [{cfg.b_lo},{cfg.b_hi}], P-256 EC-ElGamal, "
+                        f"seed {cfg.seed}",
+            "m": cfg.m, "n": cfg.n, "l": cfg.l, "w": cfg.w, "path": path, "iters": 4,
+            "parallelism": f"independent problem per GPU x{world} (no data-path collective)",
+            "l2": "flushed (256 MiB memset) before every timed step, outside the events"}
+
+
+def rank_instance_seed(cfg, rank: int) -> int:
+    """Weak scaling: every rank runs its own independent problem of the same shape
+    (no data-path exchange); rank r uses seed cfg.seed + 1000 r."""
+    return cfg.seed + 1000 * rank
+
+
+def reduce_max(value: float, dist, device) -> float:
+    """Max over ranks (the slowest rank defines the step time)."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -174,8 +200,9 @@ def run_reference(args, cfg, rank):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "l": cfg.l, "w": cfg.w, "path": args.path,
-                   "note": "ms_per_step extrapolated to the full workload from the bounded sample"},
+        "config": dict(workload_config(cfg, args.path, max(1, args.gpus)),
+                       note="oracle on host cores; each step a bounded sample (first --ref-cols output columns); "
+                            "ms_per_step extrapolated to the full workload"),
         "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -211,8 +238,9 @@ def main():
     stream = torch.cuda.current_stream()
 
     # ---- inputs (seeded, synthetic; encrypted on the GPU, outside any timing) ----
-    I = synth.make_instance(cfg, seed=cfg.seed + 1000 * rank)
-    sk, pk = P.keygen(cfg.seed + 1000 * rank)
+    seed = rank_instance_seed(cfg, rank)
+    I = synth.make_instance(cfg, seed=seed)
+    sk, pk = P.keygen(seed)
     A_h = torch.from_numpy(I.A).pin_memory()
     A = A_h.to(dev)
     ctB = P.encrypt(pk, torch.from_numpy(I.B.reshape(-1).astype(np.int32)).to(dev),
@@ -262,11 +290,7 @@ def main():
             P.profile_enable(False)
         if dist:
             dist.barrier()
-        ms = sum(a.elapsed_time(b) for a, b in evs) / K
-        if dist:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = reduce_max(sum(a.elapsed_time(b) for a, b in evs) / K, dist, dev)
         return ms, prof
 
     with ClockSampler(local) as clk:
@@ -311,11 +335,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: PC-MM {m}x{n} by {n}x{l}, w={w}{' signed' if cfg.signed else ''}, "
-                               f"B in [{cfg.b_lo},{cfg.b_hi}], P-256 EC-ElGamal, seed {cfg.seed}",
-                   "m": m, "n": n, "l": l, "w": w, "path": args.path, "iters": 4,
-                   "parallelism": f"independent problem per GPU x{world} (no data-path collective)",
-                   "l2": "flushed (256 MiB memset) before every timed step, outside the events"},
+        "config": workload_config(cfg, args.path, world),
         "point_adds_per_s": world * (acc_adds + tbl_adds + tbl_dbls) / (ms * 1e-3),
         "fp_mul_per_s": world * F_total / (ms * 1e-3),
         "roofline_whole_step": {"achieved": F_total / (ms * 1e-3) / 1e9, "peak": peak_fpmul,
