@@ -235,7 +235,7 @@ __device__ __forceinline__ void table_store(uint32_t *dst, int S, int slot, cons
     }
 }
 
-__global__ void __launch_bounds__(128) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
+__global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
                                                 int n, int l, int N, int S, uint32_t *__restrict__ tables) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
