@@ -54,7 +54,7 @@ std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- workspace
 struct Layout {
-    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, partial = 0, total = 0;
+    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, scratch = 0, partial = 0, total = 0;
     int rows = 128, ksplit = 1, slots = 16;
 };
 
@@ -87,6 +87,8 @@ Layout layout(int m, int n, int l, int w, int path) {
         off = align256(off + (size_t)n * m);
         L.tables = off;
         off = align256(off + cnt * 2 * (size_t)kPtWords * L.slots * 4);
+        L.scratch = off;
+        off = align256(off + cnt * 2 * (size_t)kPtWords * kScratchEntries * 4);
         if (ks > 1) {
             L.partial = off;
             off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
@@ -241,7 +243,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint8_t *rank = ws + L.rank;
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
-    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, tables, s));
+    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, tables, (uint32_t *)(ws + L.scratch), s));
     const int64_t cnt = (int64_t)m * l;
     if (L.ksplit == 1) {
         LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, 1, out, 0, s));

@@ -28,18 +28,48 @@ template <int S>
 struct AccumCfg {
     static constexpr int kRows = 128;
     static constexpr int kChunk = (512 / S) < 128 ? (512 / S) : 128;
-    static constexpr int kTW = kPtWords * S;                       // words per table
-    static constexpr size_t kSmem = (size_t)kChunk * kTW * 4 + (size_t)kChunk * kRows;
+    static constexpr int kTW = kPtWords * S;                       // words per table (global, entry-major)
+    static constexpr int kEW = kPtWords + 1;                       // shared-memory entry stride (odd: no conflicts)
+    static constexpr int kTWs = kEW * S;                           // words per table in shared memory
+    static constexpr size_t kSmem = (size_t)kChunk * kTWs * 4 + (size_t)kChunk * kRows;
 };
+
+// Stage one k-chunk: tables are entry-major ([slot][24 words]) in global memory;
+// shared memory pads each entry to 25 words so that lanes gathering different
+// slots hit different banks.  Rank bytes of the CTA's rows follow.  Out of line so
+// that the staging code does not perturb the hot loop's register allocation.
+template <int S>
+__device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
+                                         uint4 *smem4, uint8_t *rsm, int m, int n, int l, int c, int j, int rb,
+                                         int k0, int kc, int tid) {
+    constexpr int ROWS = AccumCfg<S>::kRows, TW = AccumCfg<S>::kTW;
+    constexpr int EW = AccumCfg<S>::kEW, TWS = AccumCfg<S>::kTWs;
+    uint32_t *tsw = reinterpret_cast<uint32_t *>(smem4);
+    for (int t = tid; t < kc * (TW / 4); t += ROWS) {
+        const int kk = t / (TW / 4), r = t % (TW / 4);
+        const int slot = r / (kPtWords / 4), q4 = (r % (kPtWords / 4)) * 4;
+        const uint4 v = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW)[r];
+        uint32_t *d = tsw + kk * TWS + slot * EW + q4;
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+    }
+    for (int t = tid; t < kc * ROWS; t += ROWS) {
+        const int row = rb * ROWS + (t % ROWS);
+        rsm[t] = row < m ? rank[(int64_t)(k0 + t / ROWS) * m + row] : (uint8_t)0;
+    }
+}
 
 template <int S>
 __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
             uint32_t *__restrict__ out, int64_t split_stride) {
     constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk, TW = AccumCfg<S>::kTW;
+    constexpr int EW = AccumCfg<S>::kEW, TWS = AccumCfg<S>::kTWs;
     extern __shared__ uint4 smem4[];
     const uint32_t *tsm = reinterpret_cast<const uint32_t *>(smem4);
-    uint8_t *rsm = reinterpret_cast<uint8_t *>(smem4) + (size_t)KCH * TW * 4;
+    uint8_t *rsm = reinterpret_cast<uint8_t *>(smem4) + (size_t)KCH * TWS * 4;
     int b = blockIdx.x;
     const int j = b % l; b /= l;
     const int c = b & 1; b >>= 1;
@@ -54,28 +84,20 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
-        for (int t = tid; t < kc * (TW / 4); t += ROWS) {
-            const int kk = t / (TW / 4), wd = t % (TW / 4);
-            const uint4 *src = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW);
-            smem4[kk * (TW / 4) + wd] = src[wd];
-        }
-        for (int t = tid; t < kc * ROWS; t += ROWS) {
-            const int row = rb * ROWS + (t % ROWS);
-            rsm[t] = row < m ? rank[(int64_t)(k0 + t / ROWS) * m + row] : (uint8_t)0;
-        }
+        stage_chunk<S>(tables, rank, smem4, rsm, m, n, l, c, j, rb, k0, kc, tid);
         __syncthreads();
         if (S <= 4) {
             // w <= 2: >= 25% zeros -- each lane walks its own nonzero entries
             int kk = 0;
             while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
             while (kk < kc) {
-                const uint32_t *T = tsm + kk * TW + rsm[kk * ROWS + tid];
+                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
                 pt Q;
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                    Q.X.v[q] = T[(0 * 8 + q) * S];
-                    Q.Y.v[q] = T[(1 * 8 + q) * S];
-                    Q.Z.v[q] = T[(2 * 8 + q) * S];
+                    Q.X.v[q] = T[0 * 8 + q];
+                    Q.Y.v[q] = T[1 * 8 + q];
+                    Q.Z.v[q] = T[2 * 8 + q];
                 }
                 pt_add_pair(acc, acc, Q);
                 kk++;
@@ -84,13 +106,13 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
         } else {
             // w >= 3: few zeros -- warp-uniform loop (a zero adds the identity in slot 0)
             for (int kk = 0; kk < kc; kk++) {
-                const uint32_t *T = tsm + kk * TW + rsm[kk * ROWS + tid];
+                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
                 pt Q;
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                    Q.X.v[q] = T[(0 * 8 + q) * S];
-                    Q.Y.v[q] = T[(1 * 8 + q) * S];
-                    Q.Z.v[q] = T[(2 * 8 + q) * S];
+                    Q.X.v[q] = T[0 * 8 + q];
+                    Q.Y.v[q] = T[1 * 8 + q];
+                    Q.Z.v[q] = T[2 * 8 + q];
                 }
                 pt_add_pair(acc, acc, Q);
             }

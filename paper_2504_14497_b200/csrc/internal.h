@@ -39,7 +39,8 @@ cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s);
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
-                          uint32_t *tables, cudaStream_t s);
+                          uint32_t *tables, uint32_t *scratch, cudaStream_t s);
+constexpr int kScratchEntries = 16;   // upper-level reconstruction scratch per (c, k, j)
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s);
 cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);

@@ -224,19 +224,46 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
 // recursive form b^(w)[u] = b^(w)[u-1] + b^(w+1)[ptr^(w)[u]] (R3, R7): levels
 // >= 2 (at most 8 entries for w <= 4) live in a small local array; level 1 is
 // produced as a running prefix sum and written straight to the table.
-constexpr int kMaxUpper = 8;
+constexpr int kMaxUpper = 8;   // entries of one level >= 2 (w <= 4: at most 7)
 
-__device__ __forceinline__ void table_store(uint32_t *dst, int S, int slot, const pt &q) {
+// Table entry (projective point) store, entry-major: 24 contiguous words per
+// slot, written as 6 x 16-byte vector stores.
+__device__ __forceinline__ void table_store(uint32_t *block, int slot, const pt &q) {
+    uint4 *d = reinterpret_cast<uint4 *>(block + slot * kPtWords);
+    d[0] = make_uint4(q.X.v[0], q.X.v[1], q.X.v[2], q.X.v[3]);
+    d[1] = make_uint4(q.X.v[4], q.X.v[5], q.X.v[6], q.X.v[7]);
+    d[2] = make_uint4(q.Y.v[0], q.Y.v[1], q.Y.v[2], q.Y.v[3]);
+    d[3] = make_uint4(q.Y.v[4], q.Y.v[5], q.Y.v[6], q.Y.v[7]);
+    d[4] = make_uint4(q.Z.v[0], q.Z.v[1], q.Z.v[2], q.Z.v[3]);
+    d[5] = make_uint4(q.Z.v[4], q.Z.v[5], q.Z.v[6], q.Z.v[7]);
+}
+
+// Upper-level scratch: entry e of (c, k, j) at words [((c n + k) 2 kMaxUpper + e) 24 + q] l + j,
+// i.e. j innermost so that a warp (32 consecutive j, same k) reads and writes
+// whole 128-byte lines; all indices are warp-uniform (same column plan).
+__device__ __forceinline__ void scr_store(uint32_t *scr, int64_t base, int e, int64_t l, const pt &q) {
+    uint32_t *d = scr + (base + (int64_t)e * kPtWords) * l;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        dst[(0 * 8 + i) * S + slot] = q.X.v[i];
-        dst[(1 * 8 + i) * S + slot] = q.Y.v[i];
-        dst[(2 * 8 + i) * S + slot] = q.Z.v[i];
+        d[(0 * 8 + i) * l] = q.X.v[i];
+        d[(1 * 8 + i) * l] = q.Y.v[i];
+        d[(2 * 8 + i) * l] = q.Z.v[i];
+    }
+}
+
+__device__ __forceinline__ void scr_load(pt &q, const uint32_t *scr, int64_t base, int e, int64_t l) {
+    const uint32_t *d = scr + (base + (int64_t)e * kPtWords) * l;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        q.X.v[i] = d[(0 * 8 + i) * l];
+        q.Y.v[i] = d[(1 * 8 + i) * l];
+        q.Z.v[i] = d[(2 * 8 + i) * l];
     }
 }
 
 __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
-                                                int n, int l, int N, int S, uint32_t *__restrict__ tables) {
+                                                   int n, int l, int N, int S, uint32_t *__restrict__ tables,
+                                                   uint32_t *__restrict__ scr) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -247,39 +274,51 @@ __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ 
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     const ColPlan pl = plans[k];
-    uint32_t *dst = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
+    uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
+    uint32_t *sj = scr + j;
+    const int64_t sbase = ((int64_t)c * n + k) * 2 * kMaxUpper * kPtWords;   // in units of l-strided words
     pt id;
     pt_identity(id);
-    table_store(dst, S, 0, id);
+    table_store(blk, 0, id);
     const int n1 = pl.n[0];
     if (N == 1) {
         for (int u = 0; u < n1; u++) {                                      // Alg. 3 line 5 only
             pt e;
             pt_mul_small_g<MulCall>(e, pl.sN[u], P);
-            table_store(dst, S, u + 1, e);
+            table_store(blk, u + 1, e);
         }
     } else {
-        pt up[kMaxUpper];                                                   // level w+1 entries
-        int nup = pl.n[N - 1];
-        for (int u = 0; u < nup; u++) pt_mul_small_g<MulCall>(up[u], pl.sN[u], P);   // line 5
-        for (int lev = N - 1; lev >= 2; lev--) {
-            pt cur[kMaxUpper];
-            const int nl = pl.n[lev - 1];
-            for (int u = 0; u < nl; u++) {
-                const pt &g = up[pl.ptr[lev - 1][u]];
-                if (u == 0) cur[0] = g;
-                else pt_add_pair(cur[u], cur[u - 1], g);                        // prefix sum
-            }
-            for (int u = 0; u < nl; u++) up[u] = cur[u];
+        // level N (Alg. 3 line 5): buffer A = entries [0, 8), buffer B = [8, 16)
+        int src = 0;
+        const int nN = pl.n[N - 1];
+        for (int u = 0; u < nN; u++) {
+            pt e;
+            pt_mul_small_g<MulCall>(e, pl.sN[u], P);
+            scr_store(sj, sbase, src + u, l, e);
         }
-        pt run = up[pl.ptr[0][0]];
-        table_store(dst, S, 1, run);
+        for (int lev = N - 1; lev >= 2; lev--) {                            // prefix sums, levels N-1 .. 2
+            const int dst = kMaxUpper - src;
+            const int nl = pl.n[lev - 1];
+            pt run, g;
+            scr_load(run, sj, sbase, src + pl.ptr[lev - 1][0], l);
+            scr_store(sj, sbase, dst, l, run);
+            for (int u = 1; u < nl; u++) {
+                scr_load(g, sj, sbase, src + pl.ptr[lev - 1][u], l);
+                pt_add_pair(run, run, g);
+                scr_store(sj, sbase, dst + u, l, run);
+            }
+            src = dst;
+        }
+        pt run, g;                                                          // level 1 -> the table
+        scr_load(run, sj, sbase, src + pl.ptr[0][0], l);
+        table_store(blk, 1, run);
         for (int u = 1; u < n1; u++) {
-            pt_add_pair(run, run, up[pl.ptr[0][u]]);                        // level-1 prefix sum
-            table_store(dst, S, u + 1, run);
+            scr_load(g, sj, sbase, src + pl.ptr[0][u], l);
+            pt_add_pair(run, run, g);
+            table_store(blk, u + 1, run);
         }
     }
-    for (int slot = n1 + 1; slot < S; slot++) table_store(dst, S, slot, id);
+    for (int slot = n1 + 1; slot < S; slot++) table_store(blk, slot, id);
 }
 
 // ------------------------------------------------------------ a5: split-k reduce
@@ -566,8 +605,8 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
 }
 
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
-                          uint32_t *tables, cudaStream_t s) {
-    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, tables);
+                          uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
+    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, tables, scratch);
     return cudaGetLastError();
 }
 
