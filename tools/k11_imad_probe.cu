@@ -44,6 +44,14 @@ __global__ void __launch_bounds__(1024, 1) probe(uint32_t *out, long long *cyc, 
             } else if (MODE == 6) { // add.cc / addc chain (IADD3 + IADD3.X)
                 asm volatile("add.cc.u32 %0, %0, %1;\n\taddc.u32 %2, %2, %3;"
                              : "+r"(a[k]), "+r"(b) : "r"(c), "r"(c));
+            } else if (MODE == 8) { // pure IMAD.WIDE.U32 (mul.wide chains, RZ addend)
+                asm volatile("{.reg .u32 t, u; mov.b64 {t, u}, %0; mul.wide.u32 %0, t, u;}" : "+l"(w[k]));
+            } else if (MODE == 9) { // IMAD.WIDE + independent IMAD (lo) chain
+                asm volatile("{.reg .u32 t, u; mov.b64 {t, u}, %0; mul.wide.u32 %0, t, u;}" : "+l"(w[k]));
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+            } else if (MODE == 10) { // IMAD.WIDE + independent IADD3 pair
+                asm volatile("{.reg .u32 t, u; mov.b64 {t, u}, %0; mul.wide.u32 %0, t, u;}" : "+l"(w[k]));
+                asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %1, %1, %0;" : "+r"(a[k]), "+r"(c));
             } else if (MODE == 7) { // madc.lo.cc / madc.hi.cc chain
                 asm volatile("mad.lo.cc.u32 %0, %0, %1, %2;\n\tmadc.hi.u32 %3, %0, %1, %3;"
                              : "+r"(a[k]), "+r"(b), "+r"(c), "+r"(*(uint32_t *)&w[k]));
@@ -94,6 +102,9 @@ int main() {
     run<5>("IMAD + 2 IADD (total instr)", 3, nsm, d_out, d_cyc);
     run<6>("add.cc+addc (total instr)", 2, nsm, d_out, d_cyc);
     run<7>("mad.lo.cc+madc.hi (ptx)", 2, nsm, d_out, d_cyc);
+    run<8>("IMAD.WIDE pure (mul.wide)", 1, nsm, d_out, d_cyc);
+    run<9>("WIDE + IMAD (total instr)", 2, nsm, d_out, d_cyc);
+    run<10>("WIDE + 2 IADD3 (total instr)", 3, nsm, d_out, d_cyc);
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
     return 0;
