@@ -154,10 +154,73 @@ __device__ __forceinline__ void pt_add_pair(pt &R, const pt &P, const pt &Q) {
     fe_add(R.Z, m13, m14);
 #endif
 }
+
+// RCB16 Algorithm 6 (doubling, a = -3) with its 13 products grouped into 6
+// independent pairs + 1 (same operations, reordered along the data flow).
+__device__ __forceinline__ void pt_dbl_pair(pt &R, const pt &P) {
+    fe b;
+    fe_b_mont(b);
+    fe t0, t1, t2, t3, z3, yz;
+    mul2(t0, P.X, P.X, t1, P.Y, P.Y);            // t0 = X^2, t1 = Y^2
+    mul2(t2, P.Z, P.Z, t3, P.X, P.Y);            // t2 = Z^2, t3 = X Y
+    mul2(z3, P.X, P.Z, yz, P.Y, P.Z);            // Z3 = X Z, t0' = Y Z (step 28)
+    fe_add(t3, t3, t3);                          // t3 = 2 X Y
+    fe_add(z3, z3, z3);                          // Z3 = 2 X Z
+    fe y3, bz;
+    mul2(y3, b, t2, bz, b, z3);                  // Y3 = b t2, Z3 = b Z3
+    fe x3, s;
+    fe_sub(y3, y3, z3);                          // Y3 = Y3 - Z3
+    fe_add(x3, y3, y3);
+    fe_add(y3, x3, y3);                          // Y3 = 3 Y3
+    fe_sub(x3, t1, y3);                          // X3 = t1 - Y3
+    fe_add(y3, t1, y3);                          // Y3 = t1 + Y3
+    fe_add(s, t2, t2);
+    fe_add(t2, t2, s);                           // t2 = 3 t2
+    fe_sub(bz, bz, t2);
+    fe_sub(bz, bz, t0);                          // Z3 = b Z3 - t2 - t0
+    fe_add(s, bz, bz);
+    fe_add(bz, bz, s);                           // Z3 = 3 Z3
+    fe_add(s, t0, t0);
+    fe_add(t0, s, t0);
+    fe_sub(t0, t0, t2);                          // t0 = 3 t0 - t2
+    fe_add(yz, yz, yz);                          // t0' = 2 Y Z
+    fe m7, m8, m10, m12;
+    mul2(m7, x3, y3, m8, x3, t3);                // Y3 = X3 Y3, X3 = X3 t3
+    mul2(m10, t0, bz, m12, yz, bz);              // t0 = t0 Z3, Z3 = t0' Z3
+    fe m13 = fe_mul_call(yz, t1);                // Z3 = t0' t1
+    fe_add(R.Y, m7, m10);                        // Y3 = Y3 + t0
+    fe_sub(R.X, m8, m12);                        // X3 = X3 - Z3
+    fe_add(m13, m13, m13);
+    fe_add(R.Z, m13, m13);                       // Z3 = 4 t0' t1
+}
+
+PCMM_HD void pt_neg(pt &R, const pt &P);
+
+// v * P for a small signed v with warp-uniform v (schoolbook): binary double-and-add
+// with the paired formulas.
+__device__ __forceinline__ void pt_mul_small_pair(pt &R, int v, const pt &P) {
+    const unsigned a = v < 0 ? (unsigned)(-v) : (unsigned)v;
+    pt acc;
+    pt_identity(acc);
+    if (a != 0) {
+        const int top = 31 - __clz(a);
+        acc = P;
+        for (int i = top - 1; i >= 0; i--) {
+            pt_dbl_pair(acc, acc);
+            if ((a >> i) & 1u) pt_add_pair(acc, acc, P);
+        }
+        if (v < 0) pt_neg(acc, acc);
+    }
+    R = acc;
+}
 #else
 template <class M> PCMM_HD void pt_add_g(pt &R, const pt &P, const pt &Q);
 struct MulInline;
 PCMM_HD void pt_add_pair(pt &R, const pt &P, const pt &Q) { pt_add_g<MulInline>(R, P, Q); }
+template <class M> PCMM_HD void pt_dbl_g(pt &R, const pt &P);
+template <class M> PCMM_HD void pt_mul_small_g(pt &R, int v, const pt &P);
+PCMM_HD void pt_dbl_pair(pt &R, const pt &P) { pt_dbl_g<MulInline>(R, P); }
+PCMM_HD void pt_mul_small_pair(pt &R, int v, const pt &P) { pt_mul_small_g<MulInline>(R, v, P); }
 #endif
 
 // RCB16 Algorithm 4: complete projective addition for a = -3.

@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(128) k_school(const int8_t *__restrict__ A, in
         if (v < lo || v > hi) { bad = true; v = 0; }
         if (v == 0) continue;                                  // 0 * ct = (inf, inf), warp-uniform
         soa_load(P, bc, cnt, (int64_t)k * l + jj);
-        pt_mul_small(T, v, P);
-        pt_add_nl(acc, acc, T);
+        pt_mul_small_pair(T, v, P);                           // one ECSM per term
+        pt_add_pair(acc, acc, T);
     }
     if (bad && lane == 0) atomicOr(status, kStatusBound);
     if (j < l) {
