@@ -29,7 +29,8 @@
  *   - Canonical ciphertext = 128 bytes C1 || C2; a point = 64 bytes x || y,
  *     each coordinate 32-byte big-endian; the point at infinity is 64 zero
  *     bytes ((0,0) is not on P-256).  Scalars are 32-byte big-endian.
- *   - Matrices are row-major: A is m x n int8 (a_ik at A[i*n + k]); Enc(B)
+ *   - Matrices are row-major: A is m x n bytes (a_ik at A[i*n + k]), read as
+ *     int8 when is_signed and as uint8 otherwise (so unsigned w = 8 reaches 255); Enc(B)
  *     is n x l canonical ciphertexts (b_kj at index k*l + j); outputs are
  *     m x l (c_ij at index i*l + j).
  *   - Signed plaintexts (is_signed = 1): a in [-2^(w-1), 2^(w-1)); a negative
@@ -124,8 +125,9 @@ PCMM_API int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, 
  *   a4  un-sort / re-insert + accumulation (Alg. 3 lines 6-9): every output
  *       gathers C_ij += T_kj[a_ik] from shared-memory table chunks.
  * Output identical (after pcmm_normalize) to pcmm_mul_schoolbook.
- * w in [1, 4] (tables of <= 15 entries per (k, j)).  Async.
- * Errors as pcmm_mul_schoolbook; ENOTSUP for w > 4 or iters outside [1, 4]. */
+ * w in [1, 8] (tables of <= 2^w - 1 entries per (k, j): w <= 4 staged in
+ * shared memory, w > 4 gathered from L2-resident global tables).  Async.
+ * Errors as pcmm_mul_schoolbook; ENOTSUP for iters outside [1, 4].        */
 PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
                     void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
 
@@ -169,11 +171,11 @@ PCMM_API int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uin
 PCMM_API int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_t *v_d, uint8_t *out_d,
                     int64_t count, void *stream);
 /* The device compression plan of Alg. 2 (step a1) for every column of A:
- * levels_d[n][4] = |a^(1)|..|a^(N)| (0 beyond N), sN_d[n][16] = values of the
- * last level, rank_d[n][m] = 1 + index of a_ik in a^(1) (0 for a_ik = 0).
- * Async; EBOUND via return after an internal synchronisation.              */
+ * levels_d[n][4] = |a^(1)|..|a^(N)| (0 beyond N), sN_d[n][256] (int16) =
+ * values of the last level, rank_d[n][m] = 1 + index of a_ik in a^(1) (0 for
+ * a_ik = 0).  w in [1, 8].  Synchronises `stream`; EBOUND on a bad entry.  */
 PCMM_API int pcmm_test_plan(const int8_t *A_d, int m, int n, int w, int is_signed, int iters, int32_t *levels_d,
-                   int8_t *sN_d, uint8_t *rank_d, void *stream);
+                   int16_t *sN_d, uint8_t *rank_d, void *stream);
 /* fp_mul throughput probe: `blocks` x `threads` threads each run `iters`
  * dependent-chain field multiplications on 4 independent chains; variant
  * selects the fe_mul implementation (0 = library default).  Writes a

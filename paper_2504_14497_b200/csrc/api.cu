@@ -55,7 +55,7 @@ std::vector<ProfRec> g_prof;
 // ---------------------------------------------------------------- workspace
 struct Layout {
     size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, scratch = 0, partial = 0, total = 0;
-    int rows = 128, ksplit = 1, slots = 16;
+    int rows = 128, ksplit = 1, slots = 16, maxup = 8;
 };
 
 Layout layout(int m, int n, int l, int w, int path) {
@@ -72,7 +72,9 @@ Layout layout(int m, int n, int l, int w, int path) {
         // ceil(base*ks / resident) / ks, plus a small charge per extra split
         // (the k_reduce additions and per-CTA chunk overheads).
         L.slots = table_slots(w);
-        const double resident = (double)num_sms() * accum_ctas_per_sm(L.slots);
+        L.maxup = max_upper(w);
+        const double resident =
+            (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(L.slots) : accum_global_ctas_per_sm());
         int ks = 1;
         double best = 1e30;
         for (int cand = 1; cand <= 16 && cand <= n; cand++) {
@@ -88,7 +90,7 @@ Layout layout(int m, int n, int l, int w, int path) {
         L.tables = off;
         off = align256(off + cnt * 2 * (size_t)kPtWords * L.slots * 4);
         L.scratch = off;
-        off = align256(off + cnt * 2 * (size_t)kPtWords * kScratchEntries * 4);
+        off = align256(off + cnt * 2 * (size_t)kPtWords * 2 * L.maxup * 4);
         if (ks > 1) {
             L.partial = off;
             off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
@@ -224,7 +226,6 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         return fail(PCMM_EINVAL, "misaligned buffer (ctB/ctC 16 B, workspace 256 B)");
     if (w < 1 || w > 8) return fail(PCMM_EINVAL, "w must be in [1, 8]");
     if (path == PCMM_PATH_CUSSEN) {
-        if (w > 4) return fail(PCMM_ENOTSUP, "Cussen path supports w <= 4 in this build");
         if (iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "iters must be in [1, 4]");
     }
     const Layout L = layout(m, n, l, w, path);
@@ -243,13 +244,17 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint8_t *rank = ws + L.rank;
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
-    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, tables, (uint32_t *)(ws + L.scratch), s));
+    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, tables, (uint32_t *)(ws + L.scratch), s));
     const int64_t cnt = (int64_t)m * l;
-    if (L.ksplit == 1) {
-        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, 1, out, 0, s));
+    uint32_t *acc_out = L.ksplit == 1 ? out : (uint32_t *)(ws + L.partial);
+    const int64_t split_stride = L.ksplit == 1 ? 0 : 2LL * kPtWords * cnt;
+    if (w <= 4) {
+        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
     } else {
+        LAUNCH("accum", s, launch_accum_global(tables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
+    }
+    if (L.ksplit > 1) {
         uint32_t *partial = (uint32_t *)(ws + L.partial);
-        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, L.ksplit, partial, 2LL * kPtWords * cnt, s));
         LAUNCH("reduce", s, launch_reduce_splits(partial, L.ksplit, cnt, out, s));
     }
     return PCMM_OK;
@@ -384,11 +389,11 @@ int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_
 }
 
 int pcmm_test_plan(const int8_t *A_d, int m, int n, int w, int is_signed, int iters, int32_t *levels_d,
-                   int8_t *sN_d, uint8_t *rank_d, void *stream) {
+                   int16_t *sN_d, uint8_t *rank_d, void *stream) {
     g_err.clear();
     int rc = check_dims(m, n, 1);
     if (rc) return rc;
-    if (w < 1 || w > 4 || iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "w in [1,4], iters in [1,4]");
+    if (w < 1 || w > 8 || iters < 1 || iters > 4) return fail(PCMM_ENOTSUP, "w in [1,8], iters in [1,4]");
     if (!A_d || !levels_d || !sN_d || !rank_d) return fail(PCMM_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)stream;
     ColPlan *plans = nullptr;
@@ -406,13 +411,13 @@ int pcmm_test_plan(const int8_t *A_d, int m, int n, int w, int is_signed, int it
     cudaFreeAsync(plans, s);
     if (e != cudaSuccess) return cuda_fail(e, "test_plan");
     std::vector<int32_t> lev((size_t)n * 4);
-    std::vector<int8_t> sn((size_t)n * 16);
+    std::vector<int16_t> sn((size_t)n * kPlanCap);
     for (int k = 0; k < n; k++) {
         for (int q = 0; q < 4; q++) lev[(size_t)k * 4 + q] = hp[k].n[q];
-        for (int q = 0; q < 16; q++) sn[(size_t)k * 16 + q] = hp[k].sN[q];
+        for (int q = 0; q < kPlanCap; q++) sn[(size_t)k * kPlanCap + q] = q < hp[k].n[iters - 1] ? hp[k].sN[q] : 0;
     }
     CK(cudaMemcpy(levels_d, lev.data(), lev.size() * 4, cudaMemcpyHostToDevice), "copy levels");
-    CK(cudaMemcpy(sN_d, sn.data(), sn.size(), cudaMemcpyHostToDevice), "copy sN");
+    CK(cudaMemcpy(sN_d, sn.data(), sn.size() * 2, cudaMemcpyHostToDevice), "copy sN");
     if (st & kStatusBound) return fail(PCMM_EBOUND, "a plaintext entry is outside its w-bit range");
     return PCMM_OK;
 }

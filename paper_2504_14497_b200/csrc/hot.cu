@@ -124,6 +124,77 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
     }
 }
 
+// ------------------------------------------------------------ a4 for w > 4: global gather
+// Tables of up to 2^w = 256 slots (24.6 KB per (k, j, c)) do not fit in shared
+// memory in useful chunks; each lane gathers its 96-byte entry straight from the
+// L2-resident tables (6 x 16-byte loads), the next entry prefetched while the
+// current addition runs.  Zero entries (slot 0) are skipped per lane.
+__device__ __forceinline__ void load_entry(pt &Q, const uint32_t *e) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(e);
+    const uint4 a = q[0], b = q[1], c = q[2], d = q[3], f = q[4], g = q[5];
+    Q.X.v[0] = a.x; Q.X.v[1] = a.y; Q.X.v[2] = a.z; Q.X.v[3] = a.w;
+    Q.X.v[4] = b.x; Q.X.v[5] = b.y; Q.X.v[6] = b.z; Q.X.v[7] = b.w;
+    Q.Y.v[0] = c.x; Q.Y.v[1] = c.y; Q.Y.v[2] = c.z; Q.Y.v[3] = c.w;
+    Q.Y.v[4] = d.x; Q.Y.v[5] = d.y; Q.Y.v[6] = d.z; Q.Y.v[7] = d.w;
+    Q.Z.v[0] = f.x; Q.Z.v[1] = f.y; Q.Z.v[2] = f.z; Q.Z.v[3] = f.w;
+    Q.Z.v[4] = g.x; Q.Z.v[5] = g.y; Q.Z.v[6] = g.z; Q.Z.v[7] = g.w;
+}
+
+constexpr int kRowsG = 128;
+
+__global__ void __launch_bounds__(kRowsG, 3)
+    k_accum_g(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int S,
+              int ksplit, uint32_t *__restrict__ out, int64_t split_stride) {
+    int b = blockIdx.x;
+    const int j = b % l; b /= l;
+    const int c = b & 1; b >>= 1;
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const int rb = b % rowblocks;
+    const int s = b / rowblocks;
+    const int i = rb * kRowsG + (int)threadIdx.x;
+    if (i >= m) return;
+    const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
+    const int64_t tstride = (int64_t)l * S * kPtWords;                   // words between consecutive k
+    const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kPtWords;
+    pt acc;
+    pt_identity(acc);
+    int k = kb;
+    while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
+    if (k < ke) {
+        pt Q;
+        load_entry(Q, tb + k * tstride + rank[(int64_t)k * m + i] * kPtWords);
+        while (true) {
+            int kn = k + 1;
+            while (kn < ke && rank[(int64_t)kn * m + i] == 0) kn++;
+            pt Qn;
+            if (kn < ke) load_entry(Qn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kPtWords);
+            pt_add_pair(acc, acc, Q);
+            if (kn >= ke) break;
+            Q = Qn;
+            k = kn;
+        }
+    }
+    const int64_t cnt = (int64_t)m * l;
+    soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, acc);
+}
+
+int accum_global_ctas_per_sm() {
+    static int occ = 0;
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum_g, kRowsG, 0) != cudaSuccess || occ <= 0)
+            occ = 3;
+    }
+    return occ;
+}
+
+cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
+    k_accum_g<<<grid, kRowsG, 0, s>>>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split);
+    return cudaGetLastError();
+}
+
 template <int VARIANT>
 __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__restrict__ out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

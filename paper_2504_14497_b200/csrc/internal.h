@@ -6,18 +6,17 @@
 
 namespace pcmm {
 
-// Per-column compression plan of Alg. 2 for w <= 4, N <= 4.
+// Per-column compression plan of Alg. 2 for w <= 8, N <= 4.
 // n[w-1] = |a^(w)| (sorted distinct nonzero values at level w, DESIGN R1);
-// sN = the level-N values (the multipliers of Alg. 3 line 5);
+// sN = the level-N values (the multipliers of Alg. 3 line 5; |v| < 640);
 // ptr[w-1][e] = index in a^(w+1) of element e of the differenced level-w vector
 // (the tracking pointer used by the un-sort / re-insert of level w+1 -> w).
+constexpr int kPlanCap = 256;         // |a^(1)| <= 255 for int8 plaintexts
 struct ColPlan {
-    int8_t n[4];
-    int8_t sN[16];
-    int8_t ptr[3][16];
+    int16_t n[4];
+    int16_t sN[kPlanCap];
+    uint8_t ptr[3][kPlanCap];
 };
-
-constexpr int kMaxVals = 15;          // |a^(1)| <= 2^w - 1 for w <= 4 (signed: 15 nonzero values)
 constexpr int kPtWords = 24;          // X, Y, Z x 8 limbs
 // table slots per (k, j, c) = 2^w (slot 0 = infinity, slots 1..|a^(1)| = entries)
 inline int table_slots(int w) { return 1 << (w < 1 ? 1 : w); }
@@ -38,9 +37,14 @@ void prof_end(cudaStream_t s);
 cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *status, cudaStream_t s);
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s);
-cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
                           uint32_t *tables, uint32_t *scratch, cudaStream_t s);
-constexpr int kScratchEntries = 16;   // upper-level reconstruction scratch per (c, k, j)
+// upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
+// kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
+inline int max_upper(int w) { return w <= 4 ? 8 : 32; }
+cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s);
+int accum_global_ctas_per_sm();
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s);
 cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);

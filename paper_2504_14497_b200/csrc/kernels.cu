@@ -152,8 +152,19 @@ __global__ void k_import(const uint8_t *__restrict__ ct, int64_t count, uint32_t
 }
 
 // ------------------------------------------------------------ a1: compression plan
-// One warp per column k of A.  Values of A lie in [-8, 15] (w <= 4), so the set
-// of distinct nonzero values of a column is a 24-bit presence mask (bit v+8).
+// One warp per column k of A (values in [-128, 255]).  Level 1: the set of
+// distinct nonzero values is a presence bitmap over [-128, 255] (12 words, bit
+// v + 128) OR-reduced across the warp; rank[k][i] = 1 + (number of set bits
+// below a_ik).  Lane 0 then builds levels 2..N the same way over [-128, 895]
+// (32-word bitmap): level w values are differences of sorted level w-1 values.
+constexpr int kBmOff = 128;
+
+__device__ __forceinline__ int bm_rank(const uint32_t *bm, int bit) {
+    int r = 0;
+    for (int q = 0; q < (bit >> 5); q++) r += __popc(bm[q]);
+    return r + __popc(bm[bit >> 5] & ((1u << (bit & 31)) - 1u));
+}
+
 __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is_signed, int N,
                        ColPlan *__restrict__ plans, uint8_t *__restrict__ rank, int *__restrict__ status) {
     int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -162,60 +173,59 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
     const int k = warp;
     const int lo = is_signed ? -(1 << (w - 1)) : 0;
     const int hi = is_signed ? (1 << (w - 1)) - 1 : (1 << w) - 1;
-    uint32_t mask = 0;
+    uint32_t bm[12];
+#pragma unroll
+    for (int q = 0; q < 12; q++) bm[q] = 0;
     bool bad = false;
     for (int i = lane; i < m; i += 32) {
-        int a = A[(int64_t)i * n + k];
+        const int a = is_signed ? (int)A[(int64_t)i * n + k] : (int)(uint8_t)A[(int64_t)i * n + k];
         if (a < lo || a > hi) bad = true;
-        else if (a != 0) mask |= 1u << (a + 8);
+        else if (a != 0) {
+            const int b = a + kBmOff;
+#pragma unroll
+            for (int q = 0; q < 12; q++)
+                if ((b >> 5) == q) bm[q] |= 1u << (b & 31);
+        }
     }
-    mask = __reduce_or_sync(0xffffffffu, mask);
+#pragma unroll
+    for (int q = 0; q < 12; q++) bm[q] = __reduce_or_sync(0xffffffffu, bm[q]);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, kStatusBound);
     // rank[k][i] = 1 + index of a_ik in the sorted distinct nonzero values (0 for a_ik = 0)
     for (int i = lane; i < m; i += 32) {
-        int a = A[(int64_t)i * n + k];
+        const int a = is_signed ? (int)A[(int64_t)i * n + k] : (int)(uint8_t)A[(int64_t)i * n + k];
         uint8_t r = 0;
-        if (a != 0 && a >= lo && a <= hi) r = (uint8_t)(1 + __popc(mask & ((1u << (a + 8)) - 1u)));
+        if (a != 0 && a >= lo && a <= hi) r = (uint8_t)(1 + bm_rank(bm, a + kBmOff));
         rank[(int64_t)k * m + i] = r;
     }
     if (lane != 0) return;
-    ColPlan P;
-#pragma unroll
-    for (int i = 0; i < 4; i++) P.n[i] = 0;
-#pragma unroll
-    for (int i = 0; i < 16; i++) { P.sN[i] = 0; P.ptr[0][i] = 0; P.ptr[1][i] = 0; P.ptr[2][i] = 0; }
-    int s[16], v[16];
+    ColPlan *P = plans + k;
+    int16_t s[kPlanCap], v[kPlanCap];
     int ns = 0;
-    for (int b = 0; b < 24; b++)
-        if ((mask >> b) & 1u) s[ns++] = b - 8;                  // level 1: sorted distinct nonzero (R1)
+    for (int b = 0; b < 12 * 32; b++)
+        if ((bm[b >> 5] >> (b & 31)) & 1u) s[ns++] = (int16_t)(b - kBmOff);   // level 1 (R1)
+    for (int q = 0; q < 4; q++) P->n[q] = 0;
     for (int lev = 1; lev <= N; lev++) {
         if (lev > 1) {
-            // sort the differenced vector v[0..nv) of level lev-1, dedupe -> s
-            int nv = ns;
-            int t[16];
-            for (int e = 0; e < nv; e++) t[e] = v[e];
-            for (int a = 1; a < nv; a++) {                      // insertion sort (<= 15 values)
-                int x = t[a], b2 = a - 1;
-                while (b2 >= 0 && t[b2] > x) { t[b2 + 1] = t[b2]; b2--; }
-                t[b2 + 1] = x;
+            // level lev: sorted distinct values of the differenced level lev-1 (v, ns entries)
+            uint32_t b2[32];
+            for (int q = 0; q < 32; q++) b2[q] = 0;
+            const int nv = ns;
+            for (int e = 0; e < nv; e++) {
+                const int b = v[e] + kBmOff;
+                b2[b >> 5] |= 1u << (b & 31);
             }
             ns = 0;
-            for (int e = 0; e < nv; e++)
-                if (ns == 0 || t[e] != s[ns - 1]) s[ns++] = t[e];
-            for (int e = 0; e < nv; e++) {                      // tracking pointers (R3)
-                int idx = 0;
-                while (s[idx] != v[e]) idx++;
-                P.ptr[lev - 2][e] = (int8_t)idx;
-            }
+            for (int b = 0; b < 32 * 32; b++)
+                if ((b2[b >> 5] >> (b & 31)) & 1u) s[ns++] = (int16_t)(b - kBmOff);
+            for (int e = 0; e < nv; e++) P->ptr[lev - 2][e] = (uint8_t)bm_rank(b2, v[e] + kBmOff);   // R3
         }
-        P.n[lev - 1] = (int8_t)ns;
+        P->n[lev - 1] = (int16_t)ns;
         if (lev < N) {                                          // differences, first element kept (R6)
-            for (int e = 0; e < ns; e++) v[e] = e == 0 ? s[0] : s[e] - s[e - 1];
+            for (int e = 0; e < ns; e++) v[e] = (int16_t)(e == 0 ? s[0] : s[e] - s[e - 1]);
         } else {
-            for (int e = 0; e < ns; e++) P.sN[e] = (int8_t)s[e];
+            for (int e = 0; e < ns; e++) P->sN[e] = s[e];
         }
     }
-    plans[k] = P;
 }
 
 // ------------------------------------------------------------ a2 + a3: tables
@@ -224,7 +234,6 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
 // recursive form b^(w)[u] = b^(w)[u-1] + b^(w+1)[ptr^(w)[u]] (R3, R7): levels
 // >= 2 (at most 8 entries for w <= 4) live in a small local array; level 1 is
 // produced as a running prefix sum and written straight to the table.
-constexpr int kMaxUpper = 8;   // entries of one level >= 2 (w <= 4: at most 7)
 
 // Table entry (projective point) store, entry-major: 24 contiguous words per
 // slot, written as 6 x 16-byte vector stores.
@@ -262,8 +271,8 @@ __device__ __forceinline__ void scr_load(pt &q, const uint32_t *scr, int64_t bas
 }
 
 __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
-                                                   int n, int l, int N, int S, uint32_t *__restrict__ tables,
-                                                   uint32_t *__restrict__ scr) {
+                                                   int n, int l, int N, int S, int maxup,
+                                                   uint32_t *__restrict__ tables, uint32_t *__restrict__ scr) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -273,10 +282,10 @@ __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ 
     const int64_t cnt = (int64_t)n * l;
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
-    const ColPlan pl = plans[k];
+    const ColPlan &pl = plans[k];
     uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
     uint32_t *sj = scr + j;
-    const int64_t sbase = ((int64_t)c * n + k) * 2 * kMaxUpper * kPtWords;   // in units of l-strided words
+    const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;   // in units of l-strided words
     pt id;
     pt_identity(id);
     table_store(blk, 0, id);
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ 
             scr_store(sj, sbase, src + u, l, e);
         }
         for (int lev = N - 1; lev >= 2; lev--) {                            // prefix sums, levels N-1 .. 2
-            const int dst = kMaxUpper - src;
+            const int dst = maxup - src;
             const int nl = pl.n[lev - 1];
             pt run, g;
             scr_load(run, sj, sbase, src + pl.ptr[lev - 1][0], l);
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(128) k_school(const int8_t *__restrict__ A, in
     pt_identity(acc);
     bool bad = false;
     for (int k = 0; k < n; k++) {
-        int v = A[(int64_t)i * n + k];
+        int v = is_signed ? (int)A[(int64_t)i * n + k] : (int)(uint8_t)A[(int64_t)i * n + k];
         if (v < lo || v > hi) { bad = true; v = 0; }
         if (v == 0) continue;                                  // 0 * ct = (inf, inf), warp-uniform
         soa_load(P, bc, cnt, (int64_t)k * l + jj);
@@ -604,9 +613,9 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
                           uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
-    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, tables, scratch);
+    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
     return cudaGetLastError();
 }
 

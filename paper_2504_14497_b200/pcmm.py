@@ -178,7 +178,9 @@ def _mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signe
         out_proj = torch.empty(proj_bytes(m * l), dtype=torch.uint8, device=A.device)
     if ws is None:
         ws = alloc_workspace(m, n, l, w, path, A.device)
-    args = (_dev(A, torch.int8, "A"), m, n, l, w, int(bool(is_signed)))
+    # A's bytes are read as int8 (is_signed) or uint8 (unsigned, w up to 8)
+    args = (_dev(A, A.dtype if A.dtype in (torch.int8, torch.uint8) else torch.int8, "A"), m, n, l, w,
+            int(bool(is_signed)))
     L = load()
     if path == SCHOOLBOOK:
         rc = L.pcmm_mul_schoolbook(*args, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
@@ -268,9 +270,10 @@ def test_point(op: int, p: torch.Tensor, q: torch.Tensor | None = None, v: torch
 def test_plan(A: torch.Tensor, w: int, is_signed: bool, iters: int = 4, stream=None):
     m, n = A.shape
     levels = torch.zeros((n, 4), dtype=torch.int32, device=A.device)
-    sN = torch.zeros((n, 16), dtype=torch.int8, device=A.device)
+    sN = torch.zeros((n, 256), dtype=torch.int16, device=A.device)
     rank = torch.zeros((n, m), dtype=torch.uint8, device=A.device)
-    _check(load().pcmm_test_plan(_dev(A, torch.int8, "A"), m, n, w, int(is_signed), iters, levels.data_ptr(),
+    _check(load().pcmm_test_plan(_dev(A, A.dtype if A.dtype in (torch.int8, torch.uint8) else torch.int8, "A"), m,
+                                 n, w, int(is_signed), iters, levels.data_ptr(),
                                  sN.data_ptr(), rank.data_ptr(), _stream(stream)))
     return levels, sN, rank
 

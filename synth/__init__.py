@@ -133,7 +133,7 @@ CONFIGS = {
 class Instance:
     cfg: Config
     x: int                 # secret key, in [1, q-1]
-    A: np.ndarray          # int8 [m, n]
+    A: np.ndarray          # [m, n] int8 (signed) or uint8 (unsigned), the boundary's byte layout
     B: np.ndarray          # int32 [n, l]
     r_be: np.ndarray       # uint8 [n*l, 32]  big-endian encryption randomness, (k, j) row-major
     x_be: bytes
@@ -149,7 +149,7 @@ def make_instance(cfg: Config, m: int | None = None, n: int | None = None, l: in
     g = SplitMix64(seed)
     x = g.scalar256()
     lo, hi = cfg.a_range
-    A = g.small(lo, hi, m * n).reshape(m, n).astype(np.int8)
+    A = g.small(lo, hi, m * n).reshape(m, n).astype(np.int8 if cfg.signed else np.uint8)
     B = g.small(cfg.b_lo, cfg.b_hi, n * l).reshape(n, l).astype(np.int32)
     r = g.scalars256(n * l)
     c = Config(cfg.name, m, n, l, cfg.w, cfg.signed, cfg.b_lo, cfg.b_hi, seed)

@@ -116,12 +116,13 @@ def test_decrypt_small():
 
 
 # ------------------------------------------------------------------ step a1: compression plan
-@pytest.mark.parametrize("w,signed", [(1, False), (2, False), (3, False), (4, False), (4, True), (2, True)])
+@pytest.mark.parametrize("w,signed", [(1, False), (2, False), (3, False), (4, False), (4, True), (2, True),
+                                      (5, False), (6, True), (8, False), (8, True)])
 def test_plan_matches_oracle(w, signed):
     g = np.random.default_rng(w * 10 + signed)
     lo, hi = (-(1 << (w - 1)), (1 << (w - 1)) - 1) if signed else (0, (1 << w) - 1)
-    m, n = 77, 40
-    A = g.integers(lo, hi + 1, (m, n)).astype(np.int8)
+    m, n = (77, 40) if w <= 4 else (300, 24)
+    A = g.integers(lo, hi + 1, (m, n)).astype(np.int8 if signed else np.uint8)
     A[:, 0] = 0                                   # all-zero column
     A[:, 1] = hi                                  # constant column
     A[::3, 2] = 0                                 # many zeros
@@ -179,10 +180,13 @@ def test_c64_config_every_output():
 
 @pytest.mark.parametrize("shape,w,signed,iters", [((100, 37, 45), 3, True, 4), ((129, 70, 33), 4, False, 4),
                                                   ((1, 1, 1), 4, False, 4), ((1, 200, 3), 4, True, 2),
-                                                  ((260, 5, 1), 2, False, 1), ((33, 64, 130), 4, True, 3)])
+                                                  ((260, 5, 1), 2, False, 1), ((33, 64, 130), 4, True, 3),
+                                                  ((140, 20, 9), 8, False, 4), ((64, 16, 40), 8, True, 4),
+                                                  ((300, 9, 5), 6, False, 2), ((50, 30, 3), 5, True, 1),
+                                                  ((256, 12, 7), 7, False, 3)])
 def test_ragged_shapes_every_output(shape, w, signed, iters):
     m, n, l = shape
-    cfg = synth.Config("ragged", m, n, l, w, signed, 0, 255, 1000 + m)
+    cfg = synth.Config("ragged", m, n, l, w, signed, 0, 255, 1000 + m + w)
     I = synth.make_instance(cfg)
     x = synth.keygen_secret(cfg.seed)
     ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
@@ -195,9 +199,9 @@ def test_degenerate_matrices():
     I = synth.make_instance(synth.CONFIGS["c64"], m=16, n=16, l=8, seed=9)
     x = synth.keygen_secret(9)
     ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
-    Z = np.zeros((16, 16), dtype=np.int8)
-    E = np.eye(16, dtype=np.int8)
-    C = np.full((16, 16), 15, dtype=np.int8)
+    Z = np.zeros((16, 16), dtype=np.uint8)
+    E = np.eye(16, dtype=np.uint8)
+    C = np.full((16, 16), 15, dtype=np.uint8)
     for path in (P.CUSSEN, P.SCHOOLBOOK):
         assert (_gpu_pcmm(Z, ct, 8, 4, False, path) == 0).all()                 # (inf, inf)
         assert (_gpu_pcmm(E, ct, 8, 4, False, path) == ct).all()                # A = I -> Enc(B)
@@ -226,7 +230,10 @@ def test_error_reporting():
         _gpu_pcmm(I.A, cbad, 8, 4, False, P.CUSSEN)
     assert e.value.code == P.PCMM_ENOTONCURVE
     with pytest.raises(P.PCMMError) as e:
-        _gpu_pcmm(I.A, ct, 8, 5, False, P.CUSSEN)
+        _gpu_pcmm(I.A, ct, 8, 9, False, P.CUSSEN)
+    assert e.value.code == P.PCMM_EINVAL
+    with pytest.raises(P.PCMMError) as e:
+        _gpu_pcmm(I.A, ct, 8, 4, False, P.CUSSEN, iters=5)
     assert e.value.code == P.PCMM_ENOTSUP
 
 

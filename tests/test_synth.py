@@ -23,7 +23,7 @@ def test_configs_ranges():
         I = synth.make_instance(cfg, m=min(cfg.m, 16), n=min(cfg.n, 16), l=min(cfg.l, 16)) if small \
             else synth.make_instance(cfg)
         lo, hi = cfg.a_range
-        assert I.A.min() >= lo and I.A.max() <= hi and I.A.dtype == np.int8
+        assert I.A.min() >= lo and I.A.max() <= hi and I.A.dtype == (np.int8 if cfg.signed else np.uint8)
         assert I.B.min() >= cfg.b_lo and I.B.max() <= cfg.b_hi
         assert 1 <= I.x < synth.P256_ORDER
         r = [int.from_bytes(v.tobytes(), "big") for v in I.r_be]
