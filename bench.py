@@ -218,11 +218,17 @@ def main():
     ap.add_argument("--ref-cols", type=int, default=48, help="output columns in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-schoolbook", action="store_true")
+    ap.add_argument("--custom", default=None, help="ad-hoc workload m,n,l,w[,signed] (A and B ranges from w / 8 bits)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     cfg = synth.CONFIGS[args.config]
+    if args.custom:
+        f = [int(x) for x in args.custom.split(",")]
+        m_, n_, l_, w_ = f[:4]
+        sg = bool(f[4]) if len(f) > 4 else False
+        cfg = synth.Config(f"custom{m_}x{n_}x{l_}w{w_}{'s' if sg else ''}", m_, n_, l_, w_, sg, 0, 255, 7)
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
 

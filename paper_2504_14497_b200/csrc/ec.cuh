@@ -155,6 +155,49 @@ __device__ __forceinline__ void pt_add_pair(pt &R, const pt &P, const pt &Q) {
 #endif
 }
 
+// RCB16 Algorithm 5: complete MIXED addition R = P + Q for a = -3 with Q affine
+// (Z2 = 1, Q != infinity): Alg. 4 with Z2 = 1, 11M + 2m_b.  The 13 products are
+// grouped into 6 independent pairs + 1.  Not on the hot path: measured in
+// k_accum it saves only 1.5 % (the loop is latency-bound), less than converting
+// the tables to affine coordinates would cost.
+__device__ __forceinline__ void pt_madd_pair(pt &R, const pt &P, const fe &X2, const fe &Y2) {
+    fe b;
+    fe_b_mont(b);
+    fe m1, m6, m2, m8, m4, m5, m7, s0, s1, y3;
+    mul2(m1, P.X, X2, m6, X2, P.Z);               // t0 = X1 X2, Y3 = X2 Z1
+    fe_add(y3, m6, P.X);                          // Y3 = X2 Z1 + X1
+    mul2(m2, P.Y, Y2, m8, b, y3);                 // t1 = Y1 Y2, Y3' = b Y3 (step 18 operand)
+    fe_add(s0, X2, Y2);
+    fe_add(s1, P.X, P.Y);
+    mul2(m4, s0, s1, m5, Y2, P.Z);                // t3 = (X2+Y2)(X1+Y1), t4 = Y2 Z1
+    m7 = fe_mul_call(b, P.Z);                     // Z3 = b Z1
+    fe t3, t4, x3, z3, t2, t0;
+    fe_add(s0, m1, m2);
+    fe_sub(t3, m4, s0);                           // t3 = t3 - (t0 + t1)
+    fe_add(t4, m5, P.Y);                          // t4 = Y2 Z1 + Y1
+    fe_sub(x3, y3, m7);                           // X3 = Y3 - Z3
+    fe_add(z3, x3, x3);
+    fe_add(x3, x3, z3);                           // X3 = 3 X3
+    fe_sub(z3, m2, x3);                           // Z3 = t1 - X3
+    fe_add(x3, m2, x3);                           // X3 = t1 + X3
+    fe_add(s0, P.Z, P.Z);
+    fe_add(t2, s0, P.Z);                          // t2 = 3 Z1
+    fe_sub(y3, m8, t2);
+    fe_sub(y3, y3, m1);                           // Y3 = b Y3 - t2 - t0
+    fe_add(s0, y3, y3);
+    fe_add(y3, s0, y3);                           // Y3 = 3 Y3
+    fe_add(s0, m1, m1);
+    fe_add(t0, s0, m1);
+    fe_sub(t0, t0, t2);                           // t0 = 3 t0 - t2
+    fe m9, m10, m11, m12, m13, m14;
+    mul2(m9, t4, y3, m10, t0, y3);                // t1 = t4 Y3, t2 = t0 Y3
+    mul2(m11, x3, z3, m12, t3, x3);               // Y3 = X3 Z3, X3 = t3 X3
+    mul2(m13, t4, z3, m14, t3, t0);               // Z3 = t4 Z3, t1 = t3 t0
+    fe_add(R.Y, m11, m10);
+    fe_sub(R.X, m12, m9);
+    fe_add(R.Z, m13, m14);
+}
+
 // RCB16 Algorithm 6 (doubling, a = -3) with its 13 products grouped into 6
 // independent pairs + 1 (same operations, reordered along the data flow).
 __device__ __forceinline__ void pt_dbl_pair(pt &R, const pt &P) {
@@ -220,6 +263,13 @@ PCMM_HD void pt_add_pair(pt &R, const pt &P, const pt &Q) { pt_add_g<MulInline>(
 template <class M> PCMM_HD void pt_dbl_g(pt &R, const pt &P);
 template <class M> PCMM_HD void pt_mul_small_g(pt &R, int v, const pt &P);
 PCMM_HD void pt_dbl_pair(pt &R, const pt &P) { pt_dbl_g<MulInline>(R, P); }
+PCMM_HD void pt_madd_pair(pt &R, const pt &P, const fe &X2, const fe &Y2) {
+    pt Q;
+    Q.X = X2;
+    Q.Y = Y2;
+    fe_one_mont(Q.Z);
+    pt_add_g<MulInline>(R, P, Q);
+}
 PCMM_HD void pt_mul_small_pair(pt &R, int v, const pt &P) { pt_mul_small_g<MulInline>(R, v, P); }
 #endif
 

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
         } else {
             // w >= 3: few zeros -- warp-uniform loop (a zero adds the identity in slot 0)
             for (int kk = 0; kk < kc; kk++) {
-                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
+                const int u = rsm[kk * ROWS + tid];
+                const uint32_t *T = tsm + kk * TWS + u * EW;
                 pt Q;
 #pragma unroll
                 for (int q = 0; q < 8; q++) {

@@ -201,8 +201,8 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
     ColPlan *P = plans + k;
     int16_t s[kPlanCap], v[kPlanCap];
     int ns = 0;
-    for (int b = 0; b < 12 * 32; b++)
-        if ((bm[b >> 5] >> (b & 31)) & 1u) s[ns++] = (int16_t)(b - kBmOff);   // level 1 (R1)
+    for (int q = 0; q < 12; q++)                                          // level 1 (R1), ascending
+        for (uint32_t x = bm[q]; x; x &= x - 1u) s[ns++] = (int16_t)(32 * q + __ffs(x) - 1 - kBmOff);
     for (int q = 0; q < 4; q++) P->n[q] = 0;
     for (int lev = 1; lev <= N; lev++) {
         if (lev > 1) {
@@ -215,8 +215,8 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
                 b2[b >> 5] |= 1u << (b & 31);
             }
             ns = 0;
-            for (int b = 0; b < 32 * 32; b++)
-                if ((b2[b >> 5] >> (b & 31)) & 1u) s[ns++] = (int16_t)(b - kBmOff);
+            for (int q = 0; q < 32; q++)
+                for (uint32_t x = b2[q]; x; x &= x - 1u) s[ns++] = (int16_t)(32 * q + __ffs(x) - 1 - kBmOff);
             for (int e = 0; e < nv; e++) P->ptr[lev - 2][e] = (uint8_t)bm_rank(b2, v[e] + kBmOff);   // R3
         }
         P->n[lev - 1] = (int16_t)ns;
