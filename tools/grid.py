@@ -1,0 +1,32 @@
+"""The paper's PC-MM grid on one B200 (NEXT-1): square n x n x n, t = w in {4, 8}
+(int8 plaintexts), Cussen vs schoolbook, next to the paper's Raspberry Pi 5 numbers
+(Table A9; speedups Table A10).
+Writes a markdown table to stdout.  Run on the GPU box."""
+import json
+import subprocess
+import sys
+
+# Table A9: (t, n) -> (Cussen s, schoolbook s) on RPi 5
+A9 = {(4, 8): (0.02, 0.06), (4, 16): (0.09, 0.49), (4, 32): (0.43, 3.93), (4, 64): (2.46, 31.43),
+      (4, 128): (14.31, 251.74), (4, 256): (95.5, 2017.64), (4, 512): (687.85, 16139.04),
+      (8, 8): (0.05, 0.08), (8, 16): (0.18, 0.63), (8, 32): (0.70, 5.02), (8, 64): (3.65, 40.13),
+      (8, 128): (20.96, 321.82), (8, 256): (139.56, 2571.89), (8, 512): (932.97, 20577.63)}
+
+rows = ["| t | n | GPU Cussen ms | GPU schoolbook ms | GPU speedup | RPi5 Cussen s | RPi5 speedup | GPU/RPi5 (Cussen) |",
+        "|---|---|---|---|---|---|---|---|"]
+for t in (4, 8):
+    for n in (8, 16, 32, 64, 128, 256, 512):
+        steps = "5" if n >= 256 else "10"
+        out = subprocess.run([sys.executable, "bench.py", "--custom", f"{n},{n},{n},{t}", "--steps", steps,
+                              "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True)
+        try:
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception:
+            rows.append(f"| {t} | {n} | error | | | | | |")
+            continue
+        cu, sb = d["ms_per_step"], d["schoolbook"]["ms_per_step"]
+        pc, ps = A9[(t, n)]
+        rows.append(f"| {t} | {n} | {cu:.3f} | {sb:.3f} | {sb / cu:.2f}x | {pc} | {ps / pc:.2f}x | "
+                    f"{pc * 1e3 / cu:.0f}x |")
+        print(rows[-1], file=sys.stderr, flush=True)
+print("\n".join(rows))
