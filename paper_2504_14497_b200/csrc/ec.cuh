@@ -49,64 +49,7 @@ __device__ __forceinline__ void mul2(fe &r0, const fe &a0, const fe &b0, fe &r1,
     r1 = r.y;
 }
 
-__device__ __forceinline__ void mul3(fe &r0, const fe &a0, const fe &b0, fe &r1, const fe &a1, const fe &b1, fe &r2,
-                                     const fe &a2, const fe &b2) {
-    fe3 r = fe_mul3_call(a0, b0, a1, b1, a2, b2);
-    r0 = r.x;
-    r1 = r.y;
-    r2 = r.z;
-}
-
-#ifndef PCMM_ADD_TRIPLES
-#define PCMM_ADD_TRIPLES 0
-#endif
-
 __device__ __forceinline__ void pt_add_pair(pt &R, const pt &P, const pt &Q) {
-#if PCMM_ADD_TRIPLES
-    // same operations as below, products grouped 3+3 / 2 / 3+3
-    fe m1, m2, m3, m4, m5, m6, s0, s1, s2, s3, b;
-    fe_b_mont(b);
-    fe_add(s0, P.X, P.Y);
-    fe_add(s1, Q.X, Q.Y);
-    mul3(m1, P.X, Q.X, m2, P.Y, Q.Y, m4, s0, s1);
-    fe_add(s0, P.Y, P.Z);
-    fe_add(s1, Q.Y, Q.Z);
-    fe_add(s2, P.X, P.Z);
-    fe_add(s3, Q.X, Q.Z);
-    mul3(m3, P.Z, Q.Z, m5, s0, s1, m6, s2, s3);
-    fe t3, t4, y3;
-    fe_add(s0, m1, m2);
-    fe_sub(t3, m4, s0);
-    fe_add(s0, m2, m3);
-    fe_sub(t4, m5, s0);
-    fe_add(s0, m1, m3);
-    fe_sub(y3, m6, s0);
-    fe m7, m8;
-    mul2(m7, b, m3, m8, b, y3);
-    fe x3, z3;
-    fe_sub(x3, y3, m7);
-    fe_add(z3, x3, x3);
-    fe_add(x3, x3, z3);
-    fe_sub(z3, m2, x3);
-    fe_add(x3, m2, x3);
-    fe t2b;
-    fe_add(s0, m3, m3);
-    fe_add(t2b, s0, m3);
-    fe_sub(y3, m8, t2b);
-    fe_sub(y3, y3, m1);
-    fe_add(s0, y3, y3);
-    fe_add(y3, s0, y3);
-    fe t0b;
-    fe_add(s0, m1, m1);
-    fe_add(t0b, s0, m1);
-    fe_sub(t0b, t0b, t2b);
-    fe m9, m10, m11, m12, m13, m14;
-    mul3(m9, t4, y3, m10, t0b, y3, m11, x3, z3);
-    mul3(m12, t3, x3, m13, t4, z3, m14, t3, t0b);
-    fe_add(R.Y, m11, m10);
-    fe_sub(R.X, m12, m9);
-    fe_add(R.Z, m13, m14);
-#else
     fe m1, m2, m3, m4, m5, m6, s0, s1, b;
     fe_b_mont(b);
     mul2(m1, P.X, Q.X, m2, P.Y, Q.Y);              // t0 = X1 X2, t1 = Y1 Y2
@@ -152,7 +95,6 @@ __device__ __forceinline__ void pt_add_pair(pt &R, const pt &P, const pt &Q) {
     fe_add(R.Y, m11, m10);
     fe_sub(R.X, m12, m9);
     fe_add(R.Z, m13, m14);
-#endif
 }
 
 // RCB16 Algorithm 5: complete MIXED addition R = P + Q for a = -3 with Q affine

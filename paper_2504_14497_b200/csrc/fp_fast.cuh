@@ -20,35 +20,6 @@
 
 #define PCMM_HAVE_FAST_MUL 1
 
-// select r = m ? x : y for a mask m in {0, 0xffffffff}: either one LOP3 per limb
-// (ALU pipe) or two IMADs per limb (FMA-heavy pipe), to balance the pipes.
-#ifndef PCMM_SEL_MUL
-#define PCMM_SEL_MUL 0
-#endif
-#ifndef PCMM_SEL_ADD
-#define PCMM_SEL_ADD 0
-#endif
-
-template <bool ON_FMA>
-__device__ __forceinline__ void sel8(uint32_t *r, const uint32_t *x, const uint32_t *y, uint32_t m) {
-    if (ON_FMA) {
-        uint32_t m01, n01;
-        asm("and.b32 %0, %2, 1;\n\tmad.lo.u32 %1, %0, 0xffffffff, 1;" : "=r"(m01), "=r"(n01) : "r"(m));
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            uint32_t t;
-            asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(x[k]), "r"(m01));
-            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[k]) : "r"(y[k]), "r"(n01), "r"(t));
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < 8; k++) r[k] = (x[k] & m) | (y[k] & ~m);
-    }
-}
-
-#ifndef PCMM_V4_ROWS
-#define PCMM_V4_ROWS 0x00   // none (V3 rows everywhere measured best)
-#endif
 
 namespace pcmm {
 
@@ -74,43 +45,9 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
         : "=r"(T[1]), "=r"(T[2]), "=r"(T[3]), "=r"(T[4]), "=r"(T[5]), "=r"(T[6]), "=r"(T[7]), "=r"(T[8])
         : "r"(l[1]), "r"(h[0]), "r"(l[2]), "r"(h[1]), "r"(l[3]), "r"(h[2]), "r"(l[4]), "r"(h[3]), "r"(l[5]),
           "r"(h[4]), "r"(l[6]), "r"(h[5]), "r"(l[7]), "r"(h[6]), "r"(h[7]));
-    // ---- rows 1..7.  Rows in PCMM_V4_ROWS skip the addend fold (no zero-extension
-    // moves on the FMA pipe) and add their low and high words with two ALU carry
-    // chains instead; the mix balances the FMA and ALU pipes.
+    // ---- rows 1..7
 #pragma unroll
     for (int i = 1; i < 8; i++) {
-        if ((PCMM_V4_ROWS >> i) & 1) {
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const uint64_t p = (uint64_t)a.v[i] * b.v[j];
-                l[j] = (uint32_t)p;
-                h[j] = (uint32_t)(p >> 32);
-            }
-            asm("add.cc.u32 %0, %0, %9;\n\t"
-                "addc.cc.u32 %1, %1, %10;\n\t"
-                "addc.cc.u32 %2, %2, %11;\n\t"
-                "addc.cc.u32 %3, %3, %12;\n\t"
-                "addc.cc.u32 %4, %4, %13;\n\t"
-                "addc.cc.u32 %5, %5, %14;\n\t"
-                "addc.cc.u32 %6, %6, %15;\n\t"
-                "addc.cc.u32 %7, %7, %16;\n\t"
-                "addc.u32 %8, 0, 0;"
-                : "+r"(T[i]), "+r"(T[i + 1]), "+r"(T[i + 2]), "+r"(T[i + 3]), "+r"(T[i + 4]), "+r"(T[i + 5]),
-                  "+r"(T[i + 6]), "+r"(T[i + 7]), "=r"(T[i + 8])
-                : "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3]), "r"(l[4]), "r"(l[5]), "r"(l[6]), "r"(l[7]));
-            asm("add.cc.u32 %0, %0, %8;\n\t"
-                "addc.cc.u32 %1, %1, %9;\n\t"
-                "addc.cc.u32 %2, %2, %10;\n\t"
-                "addc.cc.u32 %3, %3, %11;\n\t"
-                "addc.cc.u32 %4, %4, %12;\n\t"
-                "addc.cc.u32 %5, %5, %13;\n\t"
-                "addc.cc.u32 %6, %6, %14;\n\t"
-                "addc.u32 %7, %7, %15;"
-                : "+r"(T[i + 1]), "+r"(T[i + 2]), "+r"(T[i + 3]), "+r"(T[i + 4]), "+r"(T[i + 5]), "+r"(T[i + 6]),
-                  "+r"(T[i + 7]), "+r"(T[i + 8])
-                : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]));
-            continue;
-        }
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             uint64_t p = (uint64_t)a.v[i] * b.v[j] + T[i + j];
@@ -181,7 +118,8 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
         : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7]), "=r"(m)
         : "r"(T[8]), "r"(T[9]), "r"(T[10]), "r"(T[11]), "r"(T[12]), "r"(T[13]), "r"(T[14]), "r"(T[15]), "r"(E));
     // m = E - borrow: 0 -> take t (value >= p), 0xffffffff -> keep T (value < p)
-    sel8<PCMM_SEL_MUL != 0>(r.v, T + 8, t, m);
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = (T[8 + k] & m) | (t[k] & ~m);
 }
 
 // r = a + b mod p (a, b < p)
@@ -211,7 +149,8 @@ __device__ __forceinline__ void fe_add_fast(fe &r, const fe &a, const fe &b) {
         : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
           "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
     // m = carry - borrow: 0xffffffff -> a + b < p (keep s), 0 -> take s - p
-    sel8<PCMM_SEL_ADD != 0>(r.v, s, t, m);
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = (s[k] & m) | (t[k] & ~m);
 }
 
 // r = a - b mod p (a, b < p)
@@ -266,19 +205,6 @@ __device__ __noinline__ fe2 fe_mul2_call(const fe a0, const fe b0, const fe a1, 
     fe2 r;
     fe_mul_fast(r.x, a0, b0);
     fe_mul_fast(r.y, a1, b1);
-    return r;
-}
-
-struct fe3 {
-    fe x, y, z;
-};
-
-// Three independent Montgomery products in one out-of-line call.
-__device__ __noinline__ fe3 fe_mul3_call(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2, const fe b2) {
-    fe3 r;
-    fe_mul_fast(r.x, a0, b0);
-    fe_mul_fast(r.y, a1, b1);
-    fe_mul_fast(r.z, a2, b2);
     return r;
 }
 
