@@ -265,3 +265,40 @@ def test_full_size_cussen_sampled(name):
 
 def test_full_size_c256_schoolbook_sampled():
     _full_size("c256", P.SCHOOLBOOK, 16)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_and_invalid_sizes():
+    z = torch.zeros(0, dtype=torch.uint8, device="cuda")
+    assert P.normalize(torch.zeros(0, dtype=torch.uint8, device="cuda"), 0).shape == (0, 128)
+    sk, pk = P.keygen(1)
+    assert P.encrypt(pk, torch.zeros(0, dtype=torch.int32, device="cuda"), z).shape == (0, 128)
+    m, st = P.decrypt_small(sk, torch.zeros((0, 128), dtype=torch.uint8, device="cuda"), 0, 10)
+    assert m.numel() == 0 and st.numel() == 0
+    L = P.load()
+    for dims in ((0, 4, 4), (4, 0, 4), (4, 4, 0), (-1, 4, 4)):
+        rc = L.pcmm_mul_cussen(1, dims[0], dims[1], dims[2], 4, 0, 4, 16, 16, 256, 1 << 20, None)
+        assert rc == P.PCMM_EDIM
+    assert L.pcmm_workspace_bytes(4, 4, 4, 4, 1) > 0
+
+
+def test_extreme_values_and_shapes():
+    # extreme plaintexts (all max / all min signed), many rows (16 row blocks), long k (split-k)
+    for (m, n, l, w, signed) in ((2048, 6, 2, 4, False), (40, 2048, 2, 4, True), (16, 8, 3, 8, True)):
+        cfg = synth.Config("edge", m, n, l, w, signed, 0, 255, 31 + m)
+        I = synth.make_instance(cfg)
+        lo, hi = cfg.a_range
+        A = I.A.copy()
+        A[:, 0] = hi
+        A[:, 1] = lo if signed else 0
+        A[0, :] = hi
+        if signed:
+            A[1, :] = lo
+        x = synth.keygen_secret(cfg.seed)
+        ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+        out = _gpu_pcmm(A, ct, l, w, signed, P.CUSSEN)
+        sb = _gpu_pcmm(A, ct, l, w, signed, P.SCHOOLBOOK)
+        assert (out == sb).all()
+        r = I.r_be.reshape(n, l, 32)
+        for (i, j) in [(0, 0), (1, l - 1), (m - 1, 0), (m // 2, l // 2)]:
+            assert out[i * l + j].tobytes() == oracle.closed_form(x, A[i], I.B[:, j], r[:, j]), (m, n, i, j)
