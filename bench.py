@@ -213,7 +213,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c256", choices=list(synth.CONFIGS))
-    ap.add_argument("--path", default="cussen", choices=["cussen", "schoolbook"])
+    ap.add_argument("--path", default="cussen", choices=["cussen", "schoolbook", "strassen"])
+    ap.add_argument("--leaf", type=int, default=32, help="Strassen recursion leaf block size")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-cols", type=int, default=48, help="output columns in the oracle's bounded sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -254,7 +255,7 @@ def main():
     ctB_h = ctB.cpu().pin_memory()
     m, n, l, w = cfg.m, cfg.n, cfg.l, cfg.w
     count = m * l
-    path = P.CUSSEN if args.path == "cussen" else P.SCHOOLBOOK
+    path = {"cussen": P.CUSSEN, "schoolbook": P.SCHOOLBOOK, "strassen": P.STRASSEN}[args.path]
     ws = P.alloc_workspace(m, n, l, w, path, dev)
     proj = torch.empty(P.proj_bytes(count), dtype=torch.uint8, device=dev)
     out = torch.empty((count, 128), dtype=torch.uint8, device=dev)
@@ -264,6 +265,8 @@ def main():
     def step():
         if path == P.CUSSEN:
             P.mul_cussen(A, ctB, l, w, cfg.signed, 4, out_proj=proj, ws=ws)
+        elif path == P.STRASSEN:
+            P.mul_strassen(A, ctB, l, w, cfg.signed, args.leaf, out_proj=proj, ws=ws)
         else:
             P.mul_schoolbook(A, ctB, l, w, cfg.signed, out_proj=proj, ws=ws)
         P.normalize(proj, count, out=out)
@@ -362,6 +365,14 @@ def main():
         ms_sb, _ = timed(sb, max(2, args.steps // 5))
         res["schoolbook"] = {"ms_per_step": ms_sb, "value": world * count / (ms_sb * 1e-3),
                              "cussen_speedup": ms_sb / ms}
+
+        def st():
+            P.mul_strassen(A, ctB, l, w, cfg.signed, args.leaf, out_proj=proj, ws=ws_sb)
+            P.normalize(proj, count, out=out)
+        st()
+        ms_st, _ = timed(st, max(2, args.steps // 5))
+        res["strassen"] = {"ms_per_step": ms_st, "value": world * count / (ms_st * 1e-3), "leaf": args.leaf,
+                           "cussen_speedup": ms_st / ms}
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = oracle_baseline(cfg, min(args.ref_cols, cfg.l), args.path)
     if dist:

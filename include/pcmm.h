@@ -70,6 +70,7 @@ extern "C" {
 
 #define PCMM_PATH_SCHOOLBOOK 0
 #define PCMM_PATH_CUSSEN 1
+#define PCMM_PATH_STRASSEN 2
 
 /* Message for the last error on this thread ("" if none). */
 PCMM_API const char *pcmm_last_error(void);
@@ -98,7 +99,7 @@ PCMM_API int pcmm_encrypt(const uint8_t pk_h[64], const int32_t *b_d, const uint
                  void *stream);
 
 /* Workspace bytes needed by pcmm_mul_schoolbook (path 0) / pcmm_mul_cussen
- * (path 1) / pcmm_normalize (path -1, m*l = count, n = l = 1) for these
+ * (path 1) / pcmm_mul_strassen (path 2) / pcmm_normalize (path -1) for these
  * dimensions.  Returns 0 for invalid arguments.  The workspace must be device
  * memory, 256-byte aligned, and must not be used concurrently by two calls. */
 PCMM_API size_t pcmm_workspace_bytes(int m, int n, int l, int w, int path);
@@ -130,6 +131,16 @@ PCMM_API int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, 
  * Errors as pcmm_mul_schoolbook; ENOTSUP for iters outside [1, 4].        */
 PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
                     void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
+
+/* Strassen PC-MM, the paper's second comparison path (Sec. 3.1,
+ * PAPER.md:253-300): 7 half-size block PC-MMs per level (M1..M7), 5 plaintext
+ * block sums / differences (int16 internally: entries grow one bit per level)
+ * and 13 ciphertext block additions / subtractions; recursion while m, n, l are
+ * even and their halves >= `leaf`, then schoolbook on the blocks.  Output and
+ * errors as pcmm_mul_schoolbook (workspace: path 2).  Temporary blocks are
+ * allocated stream-ordered on `stream` (cudaMallocAsync).  Async.          */
+PCMM_API int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int leaf,
+                               const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
 
 /* Normalise `count` projective ciphertexts (layout above, as written by
  * pcmm_mul_*) to canonical affine bytes ctC_d[count][128] (x = X/Z, y = Y/Z,

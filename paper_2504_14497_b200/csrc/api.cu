@@ -174,7 +174,7 @@ size_t pcmm_proj_bytes(int64_t count) { return count < 0 ? 0 : (size_t)count * 2
 size_t pcmm_workspace_bytes(int m, int n, int l, int w, int path) {
     if (path == -1) return 256;
     if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 8) return 0;
-    if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN) return 0;
+    if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN && path != PCMM_PATH_STRASSEN) return 0;
     return layout(m, n, l, w, path).total;
 }
 
@@ -264,6 +264,28 @@ int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, int is_si
                         void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
     return mul_common(PCMM_PATH_SCHOOLBOOK, A_d, m, n, l, w, is_signed, 0, ctB_d, ctC_proj_d, ws_d, ws_bytes,
                       (cudaStream_t)stream);
+}
+
+int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int leaf, const uint8_t *ctB_d,
+                      void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    g_err.clear();
+    int rc = check_dims(m, n, l);
+    if (rc) return rc;
+    if (!A_d || !ctB_d || !ctC_proj_d || !ws_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)ctB_d & 15) || ((uintptr_t)ws_d & 255) || ((uintptr_t)ctC_proj_d & 15))
+        return fail(PCMM_EINVAL, "misaligned buffer (ctB/ctC 16 B, workspace 256 B)");
+    if (w < 1 || w > 8) return fail(PCMM_EINVAL, "w must be in [1, 8]");
+    if (leaf < 1) return fail(PCMM_EINVAL, "leaf must be >= 1");
+    const Layout L = layout(m, n, l, w, PCMM_PATH_STRASSEN);
+    if (ws_bytes < L.total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_workspace_bytes)");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)ws_d;
+    int *status = (int *)ws;
+    uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
+    CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
+    LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
+    LAUNCH("strassen", s, run_strassen(A_d, m, n, l, w, is_signed, bsoa, leaf, (uint32_t *)ctC_proj_d, status, s));
+    return PCMM_OK;
 }
 
 int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,

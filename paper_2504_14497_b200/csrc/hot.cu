@@ -65,7 +65,7 @@ template <int S>
 __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
             uint32_t *__restrict__ out, int64_t split_stride) {
-    constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk, TW = AccumCfg<S>::kTW;
+    constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk;
     constexpr int EW = AccumCfg<S>::kEW, TWS = AccumCfg<S>::kTWs;
     extern __shared__ uint4 smem4[];
     const uint32_t *tsm = reinterpret_cast<const uint32_t *>(smem4);

@@ -26,11 +26,11 @@ PCMM_EDECODE = -5
 PCMM_ECUDA = -6
 PCMM_ENOMEM = -7
 PCMM_ENOTSUP = -8
-SCHOOLBOOK, CUSSEN = 0, 1
+SCHOOLBOOK, CUSSEN, STRASSEN = 0, 1, 2
 
 EXPORTS = [
     "pcmm_last_error", "pcmm_version", "pcmm_proj_bytes", "pcmm_keygen", "pcmm_encrypt", "pcmm_workspace_bytes",
-    "pcmm_mul_schoolbook", "pcmm_mul_cussen", "pcmm_normalize", "pcmm_decrypt_small", "pcmm_status",
+    "pcmm_mul_schoolbook", "pcmm_mul_cussen", "pcmm_mul_strassen", "pcmm_normalize", "pcmm_decrypt_small", "pcmm_status",
     "pcmm_profile_enable", "pcmm_profile_read", "pcmm_test_field", "pcmm_test_point", "pcmm_test_plan",
     "pcmm_bench_fp_mul",
 ]
@@ -71,6 +71,7 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
             L.pcmm_workspace_bytes.argtypes = [i32] * 5
             L.pcmm_mul_schoolbook.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             L.pcmm_mul_cussen.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+            L.pcmm_mul_strassen.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             L.pcmm_normalize.argtypes = [vp, i64, vp, vp, sz, vp]
             L.pcmm_decrypt_small.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
             L.pcmm_status.argtypes = [vp, vp]
@@ -185,6 +186,9 @@ def _mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signe
     if path == SCHOOLBOOK:
         rc = L.pcmm_mul_schoolbook(*args, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
                                    ws.numel(), _stream(stream))
+    elif path == STRASSEN:
+        rc = L.pcmm_mul_strassen(*args, iters, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), _stream(stream))
     else:
         rc = L.pcmm_mul_cussen(*args, iters, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
                                ws.numel(), _stream(stream))
@@ -200,6 +204,11 @@ def mul_schoolbook(A, ctB, l, w, is_signed=False, out_proj=None, ws=None, stream
 def mul_cussen(A, ctB, l, w, is_signed=False, iters=4, out_proj=None, ws=None, stream=None):
     """Cussen PC-MM (Alg. 3) -> (projective output, workspace)."""
     return _mul(CUSSEN, A, ctB, l, w, is_signed, iters, out_proj, ws, stream)
+
+
+def mul_strassen(A, ctB, l, w, is_signed=False, leaf=32, out_proj=None, ws=None, stream=None):
+    """Strassen PC-MM down to `leaf`-sized blocks -> (projective output, workspace)."""
+    return _mul(STRASSEN, A, ctB, l, w, is_signed, leaf, out_proj, ws, stream)
 
 
 def normalize(proj: torch.Tensor, count: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -220,7 +229,8 @@ def status(ws: torch.Tensor, stream=None) -> int:
 
 def pcmm(A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signed: bool = False, path: int = CUSSEN,
          iters: int = 4, check: bool = True, stream=None) -> torch.Tensor:
-    """C = A . Enc(B) end to end on the device: mul (Cussen or schoolbook) + normalise.
+    """C = A . Enc(B) end to end on the device: mul (Cussen, schoolbook or Strassen) + normalise.
+    `iters` = Cussen's N, or Strassen's leaf block size.
     Returns canonical ciphertexts uint8 [m*l, 128] (c_ij at row i*l + j)."""
     m = A.shape[0]
     proj, ws = _mul(path, A, ctB, l, w, is_signed, iters, None, None, stream)

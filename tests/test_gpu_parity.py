@@ -302,3 +302,27 @@ def test_extreme_values_and_shapes():
         r = I.r_be.reshape(n, l, 32)
         for (i, j) in [(0, 0), (1, l - 1), (m - 1, 0), (m // 2, l // 2)]:
             assert out[i * l + j].tobytes() == oracle.closed_form(x, A[i], I.B[:, j], r[:, j]), (m, n, i, j)
+
+
+# ------------------------------------------------------------------ NEXT-3: Strassen comparison path
+@pytest.mark.parametrize("shape,w,signed,leaf", [((16, 16, 16), 4, False, 4), ((32, 32, 32), 2, False, 8),
+                                                 ((24, 40, 12), 4, True, 3), ((8, 8, 8), 8, True, 1),
+                                                 ((30, 18, 10), 3, False, 2)])
+def test_strassen_every_output(shape, w, signed, leaf):
+    m, n, l = shape
+    cfg = synth.Config("strassen", m, n, l, w, signed, 0, 255, 500 + m + w)
+    I = synth.make_instance(cfg)
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, l, w)
+    out = P.pcmm(cuda(I.A), cuda(ct), l, w, signed, path=P.STRASSEN, iters=leaf).cpu().numpy()
+    assert (out == exp).all()
+
+
+def test_strassen_c64_every_output():
+    I = synth.make_instance(synth.CONFIGS["c64"])
+    sk, pk = P.keygen(1)
+    ct = oracle.encrypt(pk, I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, 64, 4)
+    out = P.pcmm(cuda(I.A), cuda(ct), 64, 4, False, path=P.STRASSEN, iters=16).cpu().numpy()
+    assert (out == exp).all()

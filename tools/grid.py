@@ -12,21 +12,27 @@ A9 = {(4, 8): (0.02, 0.06), (4, 16): (0.09, 0.49), (4, 32): (0.43, 3.93), (4, 64
       (8, 8): (0.05, 0.08), (8, 16): (0.18, 0.63), (8, 32): (0.70, 5.02), (8, 64): (3.65, 40.13),
       (8, 128): (20.96, 321.82), (8, 256): (139.56, 2571.89), (8, 512): (932.97, 20577.63)}
 
-rows = ["| t | n | GPU Cussen ms | GPU schoolbook ms | GPU speedup | RPi5 Cussen s | RPi5 speedup | GPU/RPi5 (Cussen) |",
-        "|---|---|---|---|---|---|---|---|"]
+rows = ["| t | n | GPU Cussen ms | GPU schoolbook ms | GPU Strassen ms | speedup vs schoolbook | vs Strassen "
+        "| RPi5 Cussen s | RPi5 vs schoolbook | RPi5 vs Strassen |",
+        "|---|---|---|---|---|---|---|---|---|---|"]
+A9S = {(4, 8): 0.05, (4, 16): 0.4, (4, 32): 2.95, (4, 64): 21.73, (4, 128): 158.82, (4, 256): 1161.86,
+       (4, 512): 8480.31, (8, 8): 0.07, (8, 16): 0.48, (8, 32): 3.51, (8, 64): 25.66, (8, 128): 186.59,
+       (8, 256): 1355.63, (8, 512): 9824.45}   # Table A9 Strassen column
 for t in (4, 8):
     for n in (8, 16, 32, 64, 128, 256, 512):
         steps = "5" if n >= 256 else "10"
+        leaf = "32"   # deeper recursion leaves tiny, under-filled leaf blocks (measured slower)
         out = subprocess.run([sys.executable, "bench.py", "--custom", f"{n},{n},{n},{t}", "--steps", steps,
-                              "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True)
+                              "--warmup", "3", "--no-cpu-baseline", "--leaf", leaf], capture_output=True, text=True)
         try:
             d = json.loads(out.stdout.strip().splitlines()[-1])
         except Exception:
             rows.append(f"| {t} | {n} | error | | | | | |")
             continue
-        cu, sb = d["ms_per_step"], d["schoolbook"]["ms_per_step"]
+        cu, sb, sv = d["ms_per_step"], d["schoolbook"]["ms_per_step"], d["strassen"]["ms_per_step"]
         pc, ps = A9[(t, n)]
-        rows.append(f"| {t} | {n} | {cu:.3f} | {sb:.3f} | {sb / cu:.2f}x | {pc} | {ps / pc:.2f}x | "
-                    f"{pc * 1e3 / cu:.0f}x |")
+        pst = A9S[(t, n)]
+        rows.append(f"| {t} | {n} | {cu:.3f} | {sb:.3f} | {sv:.3f} | {sb / cu:.2f}x | {sv / cu:.2f}x | {pc} | "
+                    f"{ps / pc:.2f}x | {pst / pc:.2f}x |")
         print(rows[-1], file=sys.stderr, flush=True)
 print("\n".join(rows))
