@@ -38,7 +38,9 @@ UNIT = "entries/s"
 # IMAD pipe (IMAD.WIDE.U32 issues at half the IMAD rate; K11 probe, profiles/k11_imad.txt)
 P_PROD = 32.0
 LIMB_PRODUCTS_PER_FPMUL = 64.0
-FPMUL_PER_ADD = 14          # RCB16 Alg. 4: 12M + 2 m_b
+FPMUL_PER_ADD = 14          # RCB16 Alg. 4: 12M + 2 m_b (table build)
+FPMUL_PER_ACC_ADD = 11      # k_accum: Jacobian + affine mixed addition, 8M + 3S (squares run as products)
+FPMUL_PER_AFFINE = 6        # k_affine: 5 products per table entry + the warp-shared inversion (amortised)
 FPMUL_PER_DBL = 13          # RCB16 Alg. 6: 8M + 3S + 2 m_b
 FPMUL_PER_NORM = 6          # batch inversion + x, y + from-Montgomery (amortised)
 
@@ -114,6 +116,11 @@ def algorithmic_counts(A: np.ndarray, l: int, w: int):
     tbl_adds *= 2 * l
     tbl_dbls *= 2 * l
     return acc_adds, tbl_adds, tbl_dbls
+
+
+def table_entries(A: np.ndarray, l: int) -> int:
+    """Non-identity table entries (distinct nonzero values per column x 2 l)."""
+    return 2 * l * sum(len(np.setdiff1d(np.unique(A[:, k]), [0])) for k in range(A.shape[1]))
 
 
 class ClockSampler:
@@ -321,11 +328,12 @@ def main():
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_fpmul = nsm * P_PROD * f_max / LIMB_PRODUCTS_PER_FPMUL / 1e9          # G fp_mul/s
-    F_total = FPMUL_PER_ADD * (acc_adds + tbl_adds) + FPMUL_PER_DBL * tbl_dbls + FPMUL_PER_NORM * 2 * count
+    F_total = (FPMUL_PER_ACC_ADD * acc_adds + FPMUL_PER_ADD * tbl_adds + FPMUL_PER_DBL * tbl_dbls
+               + FPMUL_PER_AFFINE * table_entries(I.A, l) + FPMUL_PER_NORM * 2 * count)
     roof = None
     if path == P.CUSSEN and "accum" in kern:
         t_acc = kern["accum"]["ms_per_step"] + kern.get("reduce", {"ms_per_step": 0})["ms_per_step"]
-        F_acc = FPMUL_PER_ADD * acc_adds
+        F_acc = FPMUL_PER_ACC_ADD * acc_adds
         achieved = F_acc / (t_acc * 1e-3) / 1e9
         traffic = None
         try:
@@ -337,7 +345,8 @@ def main():
                 "unit": "G fp_mul/s", "frac": achieved / peak_fpmul, "traffic": traffic,
                 "peak_note": f"{nsm} SM x {P_PROD:.0f} 32x32->64 products/clk/SM x {f_max / 1e9:.3f} GHz (sm_max) "
                              f"/ 64 products per fp_mul; IMAD.WIDE half-rate measured by tools/k11_imad_probe.cu",
-                "algorithmic": f"{FPMUL_PER_ADD} fp_mul x {acc_adds} useful accumulate adds (a_ik != 0)"}
+                "algorithmic": f"{FPMUL_PER_ACC_ADD} fp_mul (8M + 3S Jacobian + affine) x {acc_adds} useful "
+                               f"accumulate adds (a_ik != 0)"}
 
     value = world * count / (ms * 1e-3)
     res = {

@@ -89,8 +89,10 @@ Layout layout(int m, int n, int l, int w, int path) {
         off = align256(off + (size_t)n * m);
         L.tables = off;
         off = align256(off + cnt * 2 * (size_t)kPtWords * L.slots * 4);
+        // upper-level scratch of k_tables, then (reused) the affine tables of k_affine
         L.scratch = off;
-        off = align256(off + cnt * 2 * (size_t)kPtWords * 2 * L.maxup * 4);
+        off = align256(off + std::max(cnt * 2 * (size_t)kPtWords * 2 * L.maxup * 4,
+                                      cnt * 2 * (size_t)kAffWords * L.slots * 4));
         if (ks > 1) {
             L.partial = off;
             off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
@@ -245,13 +247,15 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
     LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, tables, (uint32_t *)(ws + L.scratch), s));
+    uint32_t *atables = (uint32_t *)(ws + L.scratch);
+    LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s));
     const int64_t cnt = (int64_t)m * l;
     uint32_t *acc_out = L.ksplit == 1 ? out : (uint32_t *)(ws + L.partial);
     const int64_t split_stride = L.ksplit == 1 ? 0 : 2LL * kPtWords * cnt;
     if (w <= 4) {
-        LAUNCH("accum", s, launch_accum(tables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
+        LAUNCH("accum", s, launch_accum(atables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
     } else {
-        LAUNCH("accum", s, launch_accum_global(tables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
+        LAUNCH("accum", s, launch_accum_global(atables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
     }
     if (L.ksplit > 1) {
         uint32_t *partial = (uint32_t *)(ws + L.partial);

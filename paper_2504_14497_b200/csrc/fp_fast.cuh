@@ -208,4 +208,19 @@ __device__ __noinline__ fe2 fe_mul2_call(const fe a0, const fe b0, const fe a1, 
     return r;
 }
 
+struct fe3 {
+    fe x, y, z;
+};
+
+// Three independent Montgomery products in one out-of-line call (the Jacobian
+// accumulate step has a stage with three independent products).
+__device__ __noinline__ fe3 fe_mul3_call(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
+                                         const fe b2) {
+    fe3 r;
+    fe_mul_fast(r.x, a0, b0);
+    fe_mul_fast(r.y, a1, b1);
+    fe_mul_fast(r.z, a2, b2);
+    return r;
+}
+
 }  // namespace pcmm

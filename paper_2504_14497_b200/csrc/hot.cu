@@ -15,28 +15,131 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
     }
 }
 
+// ------------------------------------------------------------ Jacobian accumulator
+// The accumulate loop adds affine table entries (k_affine writes
+// the tables as (x, y)) into a Jacobian accumulator (x = X/Z^2, y = Y/Z^3) that
+// carries ZZ = Z^2: the mixed addition below is 8M + 3S with five out-of-line
+// product calls of two or three independent products each, against 12M + 2m_b
+// in seven calls for the complete homogeneous addition.  The mixed formula is
+// not complete: the identity (accumulator or entry) and H = 0 (acc = +-Q) take
+// the out-of-line general path, which runs the complete RCB16 addition
+// (ec.cuh) on homogeneous images of both points, so every input is handled.
+struct jacc {
+    fe X, Y, Z, ZZ;
+    uint32_t inf;                 // 1 while the accumulator is the identity
+};
+
+// affine table entry = 16 words (x, y); the identity has x = all ones (never a
+// residue in [0, p): p's top two words are 0xffffffff, 0x00000001)
+__device__ __forceinline__ bool aff_is_inf(const fe &x) { return (x.v[7] & x.v[6]) == 0xffffffffu; }
+
+__device__ __noinline__ jacc jac_add_slow(jacc A, const fe x2, const fe y2) {
+#ifdef __CUDA_ARCH__
+    if (aff_is_inf(x2)) return A;
+    if (A.inf) {
+        A.X = x2;
+        A.Y = y2;
+        fe_one_mont(A.Z);
+        A.ZZ = A.Z;
+        A.inf = 0;
+        return A;
+    }
+    pt P, Q, R;
+    mul2(P.X, A.X, A.Z, P.Z, A.Z, A.ZZ);          // (X Z : Y : Z^3) = the same point, homogeneous
+    P.Y = A.Y;
+    Q.X = x2;
+    Q.Y = y2;
+    fe_one_mont(Q.Z);
+    pt_add_pair(R, P, Q);                         // complete (RCB16 Alg. 4)
+    if (fe_is_zero(R.Z)) {
+        A.inf = 1;
+        return A;
+    }
+    A.Z = R.Z;                                    // back to Jacobian: (X Z, Y Z^2, Z)
+    A.ZZ = fe_mul_call(R.Z, R.Z);
+    mul2(A.X, R.X, R.Z, A.Y, R.Y, A.ZZ);
+#endif
+    return A;
+}
+
+// A += (x2, y2).  U1 = X1, S1 = Y1 (Z2 = 1): U2 = x2 Z1^2, S2 = y2 Z1^3,
+// H = U2 - X1, R = S2 - Y1, X3 = R^2 - H^3 - 2 X1 H^2,
+// Y3 = R (X1 H^2 - X3) - Y1 H^3, Z3 = Z1 H, ZZ3 = Z1^2 H^2.
+__device__ __forceinline__ void jac_add_aff(jacc &A, const fe &x2, const fe &y2) {
+#ifdef __CUDA_ARCH__
+    if (A.inf | aff_is_inf(x2)) {
+        A = jac_add_slow(A, x2, y2);
+        return;
+    }
+    fe U2, T1;
+    mul2(U2, x2, A.ZZ, T1, A.Z, A.ZZ);            // U2 = x2 ZZ, T1 = Z^3
+    fe H;
+    fe_sub(H, U2, A.X);
+    if (fe_is_zero(H)) {
+        A = jac_add_slow(A, x2, y2);
+        return;
+    }
+    fe S2, HH;
+    mul2(S2, y2, T1, HH, H, H);                   // S2 = y2 Z^3, HH = H^2
+    fe R;
+    fe_sub(R, S2, A.Y);
+    const fe3 t = fe_mul3_call(H, HH, A.X, HH, A.ZZ, HH);  // H^3, V = X1 H^2, ZZ3
+    fe R2, Z3;
+    mul2(R2, R, R, Z3, A.Z, H);                   // R^2, Z3 = Z1 H
+    fe X3, V2, D;
+    fe_add(V2, t.y, t.y);
+    fe_sub(X3, R2, t.x);
+    fe_sub(X3, X3, V2);                           // X3 = R^2 - H^3 - 2V
+    fe_sub(D, t.y, X3);
+    fe Y3a, YH;
+    mul2(Y3a, R, D, YH, A.Y, t.x);                // R (V - X3), Y1 H^3
+    fe_sub(A.Y, Y3a, YH);
+    A.X = X3;
+    A.Z = Z3;
+    A.ZZ = t.z;
+#endif
+}
+
+__device__ __forceinline__ void jac_init(jacc &A) {
+    fe_zero(A.X);
+    fe_zero(A.Y);
+    fe_zero(A.Z);
+    fe_zero(A.ZZ);
+    A.inf = 1;
+}
+
+// Jacobian -> homogeneous projective (X Z : Y : Z^3) for the output buffer
+__device__ __forceinline__ void jac_to_proj(pt &o, const jacc &A) {
+#ifdef __CUDA_ARCH__
+    if (A.inf) {
+        pt_identity(o);
+    } else {
+        mul2(o.X, A.X, A.Z, o.Z, A.Z, A.ZZ);
+        o.Y = A.Y;
+    }
+#endif
+}
+
 // ------------------------------------------------------------ a4: accumulate
 // CTA = (output column j, component c, row block, k-split).  Thread = row i.
-// Tables hold S = 2^w slots per (k, j, c) ([coord][limb][slot], slot 0 = the
-// identity), so a warp's gather for one k touches at most S consecutive banks
-// per (coord, limb): conflict-free.  Per chunk of KCH = min(128, 512/S) columns
-// the CTA stages the tables (48 KB) and the rank bytes of its rows in shared
-// memory; each lane then walks ITS OWN nonzero entries of the chunk (a_ik = 0
-// adds the identity and is skipped, R1), so a warp runs max-over-lanes
-// of the nonzero count instead of KCH additions (25% zeros at w = 2).
+// Tables hold S = 2^w affine slots per (k, j, c) (entry-major [slot][16 words],
+// slot 0 = the identity).  Per chunk of KCH = min(128, 512/S) columns the CTA
+// stages the tables and the rank bytes of its rows in shared memory (entries
+// padded to 17 words: lanes gathering different slots hit different banks);
+// each lane then walks ITS OWN nonzero entries of the chunk (a_ik = 0 adds the
+// identity and is skipped, R1), so a warp runs max-over-lanes of the
+// nonzero count instead of KCH additions (25% zeros at w = 2).
 template <int S>
 struct AccumCfg {
     static constexpr int kRows = 128;
     static constexpr int kChunk = (512 / S) < 128 ? (512 / S) : 128;
-    static constexpr int kTW = kPtWords * S;                       // words per table (global, entry-major)
-    static constexpr int kEW = kPtWords + 1;                       // shared-memory entry stride (odd: no conflicts)
+    static constexpr int kTW = kAffWords * S;                      // words per table (global, entry-major)
+    static constexpr int kEW = kAffWords + 1;                      // shared-memory entry stride (odd: no conflicts)
     static constexpr int kTWs = kEW * S;                           // words per table in shared memory
     static constexpr size_t kSmem = (size_t)kChunk * kTWs * 4 + (size_t)kChunk * kRows;
 };
 
-// Stage one k-chunk: tables are entry-major ([slot][24 words]) in global memory;
-// shared memory pads each entry to 25 words so that lanes gathering different
-// slots hit different banks.  Rank bytes of the CTA's rows follow.  Out of line so
+// Stage one k-chunk: tables and the rank bytes of the CTA's rows.  Out of line so
 // that the staging code does not perturb the hot loop's register allocation.
 template <int S>
 __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
@@ -47,7 +150,7 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
     uint32_t *tsw = reinterpret_cast<uint32_t *>(smem4);
     for (int t = tid; t < kc * (TW / 4); t += ROWS) {
         const int kk = t / (TW / 4), r = t % (TW / 4);
-        const int slot = r / (kPtWords / 4), q4 = (r % (kPtWords / 4)) * 4;
+        const int slot = r / (kAffWords / 4), q4 = (r % (kAffWords / 4)) * 4;
         const uint4 v = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW)[r];
         uint32_t *d = tsw + kk * TWS + slot * EW + q4;
         d[0] = v.x;
@@ -79,66 +182,49 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
     const int tid = (int)threadIdx.x;
     const int i = rb * ROWS + tid;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
-    pt acc;
-    pt_identity(acc);
+    jacc acc;
+    jac_init(acc);
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
         stage_chunk<S>(tables, rank, smem4, rsm, m, n, l, c, j, rb, k0, kc, tid);
         __syncthreads();
-        if (S <= 4) {
-            // w <= 2: >= 25% zeros -- each lane walks its own nonzero entries
-            int kk = 0;
+        // each lane walks its own nonzero entries (zeros are the identity, skipped)
+        int kk = 0;
+        while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
+        while (kk < kc) {
+            const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
+            fe x2, y2;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                x2.v[q] = T[q];
+                y2.v[q] = T[8 + q];
+            }
+            jac_add_aff(acc, x2, y2);
+            kk++;
             while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
-            while (kk < kc) {
-                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
-                pt Q;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    Q.X.v[q] = T[0 * 8 + q];
-                    Q.Y.v[q] = T[1 * 8 + q];
-                    Q.Z.v[q] = T[2 * 8 + q];
-                }
-                pt_add_pair(acc, acc, Q);
-                kk++;
-                while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
-            }
-        } else {
-            // w >= 3: few zeros -- warp-uniform loop (a zero adds the identity in slot 0)
-            for (int kk = 0; kk < kc; kk++) {
-                const int u = rsm[kk * ROWS + tid];
-                const uint32_t *T = tsm + kk * TWS + u * EW;
-                pt Q;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    Q.X.v[q] = T[0 * 8 + q];
-                    Q.Y.v[q] = T[1 * 8 + q];
-                    Q.Z.v[q] = T[2 * 8 + q];
-                }
-                pt_add_pair(acc, acc, Q);
-            }
         }
     }
     if (i < m) {
         const int64_t cnt = (int64_t)m * l;
-        soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, acc);
+        pt o;
+        jac_to_proj(o, acc);
+        soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
     }
 }
 
 // ------------------------------------------------------------ a4 for w > 4: global gather
-// Tables of up to 2^w = 256 slots (24.6 KB per (k, j, c)) do not fit in shared
-// memory in useful chunks; each lane gathers its 96-byte entry straight from the
-// L2-resident tables (6 x 16-byte loads), the next entry prefetched while the
+// Tables of up to 2^w = 256 slots (16 KB per (k, j, c)) do not fit in shared
+// memory in useful chunks; each lane gathers its 64-byte entry straight from the
+// L2-resident tables (4 x 16-byte loads), the next entry prefetched while the
 // current addition runs.  Zero entries (slot 0) are skipped per lane.
-__device__ __forceinline__ void load_entry(pt &Q, const uint32_t *e) {
+__device__ __forceinline__ void load_aff(fe &x, fe &y, const uint32_t *e) {
     const uint4 *q = reinterpret_cast<const uint4 *>(e);
-    const uint4 a = q[0], b = q[1], c = q[2], d = q[3], f = q[4], g = q[5];
-    Q.X.v[0] = a.x; Q.X.v[1] = a.y; Q.X.v[2] = a.z; Q.X.v[3] = a.w;
-    Q.X.v[4] = b.x; Q.X.v[5] = b.y; Q.X.v[6] = b.z; Q.X.v[7] = b.w;
-    Q.Y.v[0] = c.x; Q.Y.v[1] = c.y; Q.Y.v[2] = c.z; Q.Y.v[3] = c.w;
-    Q.Y.v[4] = d.x; Q.Y.v[5] = d.y; Q.Y.v[6] = d.z; Q.Y.v[7] = d.w;
-    Q.Z.v[0] = f.x; Q.Z.v[1] = f.y; Q.Z.v[2] = f.z; Q.Z.v[3] = f.w;
-    Q.Z.v[4] = g.x; Q.Z.v[5] = g.y; Q.Z.v[6] = g.z; Q.Z.v[7] = g.w;
+    const uint4 a = q[0], b = q[1], c = q[2], d = q[3];
+    x.v[0] = a.x; x.v[1] = a.y; x.v[2] = a.z; x.v[3] = a.w;
+    x.v[4] = b.x; x.v[5] = b.y; x.v[6] = b.z; x.v[7] = b.w;
+    y.v[0] = c.x; y.v[1] = c.y; y.v[2] = c.z; y.v[3] = c.w;
+    y.v[4] = d.x; y.v[5] = d.y; y.v[6] = d.z; y.v[7] = d.w;
 }
 
 constexpr int kRowsG = 128;
@@ -155,28 +241,31 @@ __global__ void __launch_bounds__(kRowsG, 3)
     const int i = rb * kRowsG + (int)threadIdx.x;
     if (i >= m) return;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
-    const int64_t tstride = (int64_t)l * S * kPtWords;                   // words between consecutive k
-    const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kPtWords;
-    pt acc;
-    pt_identity(acc);
+    const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive k
+    const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kAffWords;
+    jacc acc;
+    jac_init(acc);
     int k = kb;
     while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
     if (k < ke) {
-        pt Q;
-        load_entry(Q, tb + k * tstride + rank[(int64_t)k * m + i] * kPtWords);
+        fe x2, y2;
+        load_aff(x2, y2, tb + k * tstride + rank[(int64_t)k * m + i] * kAffWords);
         while (true) {
             int kn = k + 1;
             while (kn < ke && rank[(int64_t)kn * m + i] == 0) kn++;
-            pt Qn;
-            if (kn < ke) load_entry(Qn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kPtWords);
-            pt_add_pair(acc, acc, Q);
+            fe xn, yn;
+            if (kn < ke) load_aff(xn, yn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kAffWords);
+            jac_add_aff(acc, x2, y2);
             if (kn >= ke) break;
-            Q = Qn;
+            x2 = xn;
+            y2 = yn;
             k = kn;
         }
     }
     const int64_t cnt = (int64_t)m * l;
-    soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, acc);
+    pt o;
+    jac_to_proj(o, acc);
+    soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
 }
 
 int accum_global_ctas_per_sm() {

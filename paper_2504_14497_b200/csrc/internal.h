@@ -18,6 +18,7 @@ struct ColPlan {
     uint8_t ptr[3][kPlanCap];
 };
 constexpr int kPtWords = 24;          // X, Y, Z x 8 limbs
+constexpr int kAffWords = 16;         // affine table entry: x, y x 8 limbs (identity: x = all ones)
 // table slots per (k, j, c) = 2^w (slot 0 = infinity, slots 1..|a^(1)| = entries)
 inline int table_slots(int w) { return 1 << (w < 1 ? 1 : w); }
 
@@ -39,6 +40,8 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
                         int *status, cudaStream_t s);
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
                           uint32_t *tables, uint32_t *scratch, cudaStream_t s);
+// homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
+cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s);
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
 // kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
 inline int max_upper(int w) { return w <= 4 ? 8 : 32; }

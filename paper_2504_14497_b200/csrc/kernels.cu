@@ -14,6 +14,8 @@
 //   k_encrypt / k_pubkey / k_dlog_table / k_decrypt: boundary
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "ec.cuh"
 #include "internal.h"
 
@@ -330,6 +332,114 @@ __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ 
     for (int slot = n1 + 1; slot < S; slot++) table_store(blk, slot, id);
 }
 
+// ------------------------------------------------------------ a3': tables -> affine
+// The accumulate loop adds table entries with the Jacobian + affine mixed
+// addition (hot.cu), so the tables are converted once to affine (x, y) =
+// (X/Z, Y/Z) with Montgomery's simultaneous inversion: each thread takes 2 x
+// `pairs` entries (stride = grid size, so a warp reads consecutive entries) as
+// two interleaved product chains (independent products: twice the ILP), one
+// fe_inv per thread, 5 products per entry.  The prefix products are parked in
+// the output's y words between the two passes.  Identity entries (Z = 0:
+// slot 0 and unused slots) become x = all ones (hot.cu aff_is_inf).
+struct AffIn {
+    fe z;
+    bool ok;        // entry exists and Z != 0
+};
+
+__device__ __forceinline__ AffIn aff_load_z(const uint32_t *__restrict__ tab, int64_t e, int64_t entries) {
+    AffIn a;
+    a.ok = false;
+    fe_one_mont(a.z);
+    if (e < entries) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(tab + e * kPtWords);
+        const uint4 z0 = src[4], z1 = src[5];
+        if ((z0.x | z0.y | z0.z | z0.w | z1.x | z1.y | z1.z | z1.w) != 0) {
+            a.z = fe{{z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w}};
+            a.ok = true;
+        }
+    }
+    return a;
+}
+
+__device__ __forceinline__ void aff_pass1_store(uint32_t *__restrict__ atab, int64_t e, int64_t entries,
+                                                const AffIn &a, const fe &prefix) {
+    if (e >= entries) return;
+    uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
+    if (!a.ok) {
+        const uint4 ones = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        dst[0] = ones;
+        dst[1] = ones;
+        dst[2] = make_uint4(0, 0, 0, 0);
+        dst[3] = make_uint4(0, 0, 0, 0);
+    } else {
+        dst[2] = make_uint4(prefix.v[0], prefix.v[1], prefix.v[2], prefix.v[3]);
+        dst[3] = make_uint4(prefix.v[4], prefix.v[5], prefix.v[6], prefix.v[7]);
+    }
+}
+
+__device__ __forceinline__ void aff_pass2_store(const uint32_t *__restrict__ tab, uint32_t *__restrict__ atab,
+                                                int64_t e, const fe &zi) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(tab + e * kPtWords);
+    uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
+    const uint4 x0 = src[0], x1 = src[1], y0 = src[2], y1 = src[3];
+    const fe X = {{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
+    const fe Y = {{y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w}};
+    fe x, y;
+    fe_mul(x, X, zi);
+    fe_mul(y, Y, zi);
+    dst[0] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+    dst[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+    dst[2] = make_uint4(y.v[0], y.v[1], y.v[2], y.v[3]);
+    dst[3] = make_uint4(y.v[4], y.v[5], y.v[6], y.v[7]);
+}
+
+__device__ __forceinline__ fe aff_prefix(const uint32_t *__restrict__ atab, int64_t e) {
+    const uint4 *d = reinterpret_cast<const uint4 *>(atab + e * kAffWords);
+    const uint4 p0 = d[2], p1 = d[3];
+    return fe{{p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w}};
+}
+
+__global__ void __launch_bounds__(128) k_affine(const uint32_t *__restrict__ tab, int64_t entries, int pairs,
+                                               uint32_t *__restrict__ atab) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= entries) return;
+    fe acc0, acc1;
+    fe_one_mont(acc0);
+    acc1 = acc0;
+    for (int r = 0; r < pairs; r++) {             // chain 0: entries t + 2rT, chain 1: t + (2r+1)T
+        const int64_t e0 = t + (2 * r) * T, e1 = e0 + T;
+        if (e0 >= entries) break;
+        const AffIn a0 = aff_load_z(tab, e0, entries), a1 = aff_load_z(tab, e1, entries);
+        aff_pass1_store(atab, e0, entries, a0, acc0);
+        aff_pass1_store(atab, e1, entries, a1, acc1);
+        fe n0, n1;
+        fe_mul(n0, acc0, a0.z);
+        fe_mul(n1, acc1, a1.z);
+        acc0 = n0;
+        acc1 = n1;
+    }
+    fe tot, inv, inv0, inv1;
+    fe_mul(tot, acc0, acc1);
+    fe_inv(inv, tot);
+    fe_mul(inv0, inv, acc1);                      // 1 / acc0
+    fe_mul(inv1, inv, acc0);                      // 1 / acc1
+    for (int r = pairs - 1; r >= 0; r--) {
+        const int64_t e0 = t + (2 * r) * T, e1 = e0 + T;
+        if (e0 >= entries) continue;
+        const AffIn a0 = aff_load_z(tab, e0, entries), a1 = aff_load_z(tab, e1, entries);
+        fe zi0, zi1, n0, n1;
+        if (a0.ok) fe_mul(zi0, inv0, aff_prefix(atab, e0));
+        if (a1.ok) fe_mul(zi1, inv1, aff_prefix(atab, e1));
+        fe_mul(n0, inv0, a0.z);
+        fe_mul(n1, inv1, a1.z);
+        inv0 = n0;
+        inv1 = n1;
+        if (a0.ok) aff_pass2_store(tab, atab, e0, zi0);
+        if (a1.ok) aff_pass2_store(tab, atab, e1, zi1);
+    }
+}
+
 // ------------------------------------------------------------ a5: split-k reduce
 __global__ void k_reduce(const uint32_t *__restrict__ partial, int ksplit, int64_t count, uint32_t *__restrict__ out) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -610,6 +720,22 @@ cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s) {
     k_plan<<<blocks_for((int64_t)n * 32, 128), 128, 0, s>>>(A, m, n, w, is_signed, N, plans, rank, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s) {
+    if (entries <= 0) return cudaSuccess;
+    // up to 2 x 32 entries per thread (the inversion amortised over 64), but at
+    // least one CTA per SM (measured at 256^3: 32 pairs 0.47 ms, 16 0.51, 8 0.65)
+    static int pairs_env = -1;
+    if (pairs_env < 0) {
+        const char *e = getenv("PCMM_AFFINE_PAIRS");
+        pairs_env = e ? atoi(e) : 0;
+    }
+    const int64_t want = (int64_t)num_sms() * 128;
+    int pairs = pairs_env > 0 ? pairs_env : (int)std::min<int64_t>(32, std::max<int64_t>(1, entries / (2 * want)));
+    const int64_t threads = (entries + 2 * pairs - 1) / (2 * pairs);
+    k_affine<<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, pairs, atables);
     return cudaGetLastError();
 }
 

@@ -214,6 +214,39 @@ def test_degenerate_matrices():
     assert (_gpu_pcmm(I.A, ct2, 8, 4, False, P.CUSSEN) == exp).all()
 
 
+@pytest.mark.parametrize("w", [4, 6])
+def test_accumulator_exceptional_cases(w):
+    # Equal ciphertexts in rows k = 0..3 make the accumulated sum equal to +-(the next
+    # table entry): the Jacobian + affine mixed addition of the accumulate kernel hits
+    # H = 0 (doubling, and cancellation to the identity followed by more additions),
+    # which its general path must handle.  w = 4: shared-memory kernel, w = 6: the
+    # global-gather kernel.
+    m, n, l = 8, 8, 4
+    I = synth.make_instance(synth.CONFIGS["c64"], m=m, n=n, l=l, seed=21)
+    x = synth.keygen_secret(21)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct[1] = ct[0]
+    ct[2] = ct[0]
+    ct[3] = ct[0]
+    ct = np.ascontiguousarray(ct.reshape(n * l, 128))
+    A = np.array([[1, 1, 0, 0, 3, 2, 1, 0],          # Q + Q
+                  [1, -1, 0, 0, 5, 0, 0, 2],         # Q - Q = identity, then more
+                  [2, 0, -2, 0, 0, 0, 0, 1],         # 2Q - 2Q
+                  [1, 1, -2, 0, 0, 0, 0, 0],         # Q + Q - 2Q = identity at the end
+                  [3, -1, -2, 0, 0, 1, 0, 0],
+                  [-1, -1, -1, 3, 0, 0, 0, 0],       # -Q - Q - Q + 3Q
+                  [7, -8, 1, 0, 1, 1, 1, 1],
+                  [-8, 7, 1, 1, -1, 2, -3, 4]], dtype=np.int8)
+    if w == 6:
+        A = A.astype(np.int16) * 3
+        A[6, 0], A[6, 1] = 31, -32
+        A = A.astype(np.int8)
+    exp, _ = oracle.pcmm(oracle.SCHOOLBOOK, A, ct, l, w)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(A, ct, l, w, True, path) == exp).all(), path
+    assert (exp[3 * l:4 * l] == 0).all()            # row 3 sums to the identity in every column
+
+
 def test_error_reporting():
     I = synth.make_instance(synth.CONFIGS["c64"], m=8, n=8, l=8, seed=3)
     x = synth.keygen_secret(3)
