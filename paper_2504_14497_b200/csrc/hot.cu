@@ -165,7 +165,7 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
 }
 
 template <int S>
-__global__ void __launch_bounds__(AccumCfg<S>::kRows, 3)
+__global__ void __launch_bounds__(AccumCfg<S>::kRows, 4)
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
             uint32_t *__restrict__ out, int64_t split_stride) {
     constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk;
