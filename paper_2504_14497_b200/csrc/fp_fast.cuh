@@ -23,8 +23,8 @@
 
 namespace pcmm {
 
-__device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
-    uint32_t T[17];
+// operand scanning (V3): IMAD.WIDE folds the running column word; per-row add chain
+__device__ __forceinline__ void fe_prod_os(uint32_t T[16], const fe &a, const fe &b) {
     uint32_t l[8], h[8];
     // ---- row 0
 #pragma unroll
@@ -68,6 +68,117 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
             : "r"(l[1]), "r"(h[0]), "r"(l[2]), "r"(h[1]), "r"(l[3]), "r"(h[2]), "r"(l[4]), "r"(h[3]), "r"(l[5]),
               "r"(h[4]), "r"(l[6]), "r"(h[5]), "r"(l[7]), "r"(h[6]), "r"(h[7]));
     }
+}
+
+// Even/odd product scanning: the 64 products a_j b_i are summed into two
+// accumulators, E (products at even word offsets, i + j even) and O (odd
+// offsets, stored one word down so that its pairs are aligned too).  A row i of
+// either accumulator is a chain of four mad.lo.cc / madc.hi.cc pairs, which
+// ptxas fuses into IMAD.WIDE.U32(.X) with the aligned 64-bit accumulator pair as
+// addend and the carry in a predicate: no zeroed high words and no separate add
+// chain per row.  The carry out of a chain lands in the word above it, which
+// holds at most earlier carries (never a product word) at that point, so
+// `addc` there cannot overflow.  T = E + O 2^32 at the end (one add chain).
+#define PCMM_CHAIN4C(d0, d1, d2, d3, d4, d5, d6, d7, c, x0, x1, x2, x3, y)                        \
+    asm("mad.lo.cc.u32 %0, %9, %13, %0;\n\t"                                                      \
+        "madc.hi.cc.u32 %1, %9, %13, %1;\n\t"                                                     \
+        "madc.lo.cc.u32 %2, %10, %13, %2;\n\t"                                                    \
+        "madc.hi.cc.u32 %3, %10, %13, %3;\n\t"                                                    \
+        "madc.lo.cc.u32 %4, %11, %13, %4;\n\t"                                                    \
+        "madc.hi.cc.u32 %5, %11, %13, %5;\n\t"                                                    \
+        "madc.lo.cc.u32 %6, %12, %13, %6;\n\t"                                                    \
+        "madc.hi.cc.u32 %7, %12, %13, %7;\n\t"                                                    \
+        "addc.u32 %8, %8, 0;"                                                                     \
+        : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3), "+r"(d4), "+r"(d5), "+r"(d6), "+r"(d7), "+r"(c) \
+        : "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(y))
+#define PCMM_CHAIN4(d0, d1, d2, d3, d4, d5, d6, d7, x0, x1, x2, x3, y)                            \
+    asm("mad.lo.cc.u32 %0, %8, %12, %0;\n\t"                                                      \
+        "madc.hi.cc.u32 %1, %8, %12, %1;\n\t"                                                     \
+        "madc.lo.cc.u32 %2, %9, %12, %2;\n\t"                                                     \
+        "madc.hi.cc.u32 %3, %9, %12, %3;\n\t"                                                     \
+        "madc.lo.cc.u32 %4, %10, %12, %4;\n\t"                                                    \
+        "madc.hi.cc.u32 %5, %10, %12, %5;\n\t"                                                    \
+        "madc.lo.cc.u32 %6, %11, %12, %6;\n\t"                                                    \
+        "madc.hi.u32 %7, %11, %12, %7;"                                                           \
+        : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3), "+r"(d4), "+r"(d5), "+r"(d6), "+r"(d7)          \
+        : "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(y))
+
+__device__ __forceinline__ void fe_prod_eo(uint32_t T[16], const fe &a, const fe &b) {
+    uint32_t E[16], O[16];                       // O[k] = word k + 1
+    // row 0: plain products
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const uint64_t pe = (uint64_t)a.v[2 * j] * b.v[0];
+        const uint64_t po = (uint64_t)a.v[2 * j + 1] * b.v[0];
+        E[2 * j] = (uint32_t)pe;
+        E[2 * j + 1] = (uint32_t)(pe >> 32);
+        O[2 * j] = (uint32_t)po;
+        O[2 * j + 1] = (uint32_t)(po >> 32);
+    }
+#pragma unroll
+    for (int k = 8; k < 16; k++) {
+        E[k] = 0;
+        O[k] = 0;
+    }
+    const uint32_t a0 = a.v[0], a1 = a.v[1], a2 = a.v[2], a3 = a.v[3];
+    const uint32_t a4 = a.v[4], a5 = a.v[5], a6 = a.v[6], a7 = a.v[7];
+#pragma unroll
+    for (int i = 1; i < 8; i++) {
+        const uint32_t bi = b.v[i];
+        if (i & 1) {
+            // even a-limbs -> odd offsets i..i+7 = O[i-1..i+6], carry O[i+7]
+            PCMM_CHAIN4C(O[i - 1], O[i], O[i + 1], O[i + 2], O[i + 3], O[i + 4], O[i + 5], O[i + 6], O[i + 7],
+                         a0, a2, a4, a6, bi);
+            // odd a-limbs -> even offsets i+1..i+8 = E[i+1..i+8], carry E[i+9] (none for i = 7)
+            if (i < 7) {
+                PCMM_CHAIN4C(E[i + 1], E[i + 2], E[i + 3], E[i + 4], E[i + 5], E[i + 6], E[i + 7], E[i + 8],
+                             E[(i + 9) & 15], a1, a3, a5, a7, bi);
+            } else {
+                PCMM_CHAIN4(E[8], E[9], E[10], E[11], E[12], E[13], E[14], E[15], a1, a3, a5, a7, bi);
+            }
+        } else {
+            // even a-limbs -> even offsets E[i..i+7], carry E[i+8]
+            PCMM_CHAIN4C(E[i], E[i + 1], E[i + 2], E[i + 3], E[i + 4], E[i + 5], E[i + 6], E[i + 7], E[i + 8],
+                         a0, a2, a4, a6, bi);
+            // odd a-limbs -> odd offsets i+1..i+8 = O[i..i+7], carry O[i+8]
+            PCMM_CHAIN4C(O[i], O[i + 1], O[i + 2], O[i + 3], O[i + 4], O[i + 5], O[i + 6], O[i + 7], O[i + 8],
+                         a1, a3, a5, a7, bi);
+        }
+    }
+    // T = E + O 2^32 (< 2^512: no carry out of word 15)
+    T[0] = E[0];
+    asm("add.cc.u32 %0, %15, %30;\n\t"
+        "addc.cc.u32 %1, %16, %31;\n\t"
+        "addc.cc.u32 %2, %17, %32;\n\t"
+        "addc.cc.u32 %3, %18, %33;\n\t"
+        "addc.cc.u32 %4, %19, %34;\n\t"
+        "addc.cc.u32 %5, %20, %35;\n\t"
+        "addc.cc.u32 %6, %21, %36;\n\t"
+        "addc.cc.u32 %7, %22, %37;\n\t"
+        "addc.cc.u32 %8, %23, %38;\n\t"
+        "addc.cc.u32 %9, %24, %39;\n\t"
+        "addc.cc.u32 %10, %25, %40;\n\t"
+        "addc.cc.u32 %11, %26, %41;\n\t"
+        "addc.cc.u32 %12, %27, %42;\n\t"
+        "addc.cc.u32 %13, %28, %43;\n\t"
+        "addc.u32 %14, %29, %44;"
+        : "=r"(T[1]), "=r"(T[2]), "=r"(T[3]), "=r"(T[4]), "=r"(T[5]), "=r"(T[6]), "=r"(T[7]), "=r"(T[8]),
+          "=r"(T[9]), "=r"(T[10]), "=r"(T[11]), "=r"(T[12]), "=r"(T[13]), "=r"(T[14]), "=r"(T[15])
+        : "r"(E[1]), "r"(E[2]), "r"(E[3]), "r"(E[4]), "r"(E[5]), "r"(E[6]), "r"(E[7]), "r"(E[8]), "r"(E[9]),
+          "r"(E[10]), "r"(E[11]), "r"(E[12]), "r"(E[13]), "r"(E[14]), "r"(E[15]),
+          "r"(O[0]), "r"(O[1]), "r"(O[2]), "r"(O[3]), "r"(O[4]), "r"(O[5]), "r"(O[6]), "r"(O[7]), "r"(O[8]),
+          "r"(O[9]), "r"(O[10]), "r"(O[11]), "r"(O[12]), "r"(O[13]), "r"(O[14]));
+}
+
+#ifndef PCMM_MUL_PRODUCT
+#define PCMM_MUL_PRODUCT 1        // 1: even/odd product scanning, 0: operand scanning
+#endif
+
+template <int PV>
+__device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
+    uint32_t T[16];
+    if (PV == 1) fe_prod_eo(T, a, b);
+    else fe_prod_os(T, a, b);
     // ---- reduction, 64-bit quotient digits: -p^-1 = 1 mod 2^64 (p = -1 mod 2^96),
     // so round r (base b = 2r) takes q = T[b] + 2^32 T[b+1] and adds
     //   q p 2^(32b) = -q + q 2^96 + u 2^192,  u = q (2^64 - 2^32 + 1) < 2^128.
@@ -121,6 +232,8 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) {
 #pragma unroll
     for (int k = 0; k < 8; k++) r.v[k] = (T[8 + k] & m) | (t[k] & ~m);
 }
+
+__device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) { fe_mul_fast_v<PCMM_MUL_PRODUCT>(r, a, b); }
 
 // r = a + b mod p (a, b < p)
 __device__ __forceinline__ void fe_add_fast(fe &r, const fe &a, const fe &b) {

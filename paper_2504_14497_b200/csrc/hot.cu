@@ -300,6 +300,9 @@ __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__res
         for (int c = 0; c < 4; c++) {
             if (VARIANT == 1) fe_mul_portable(x[c], x[c], y);
             else if (VARIANT == 2) fe_add(x[c], x[c], y);
+#ifdef __CUDA_ARCH__
+            else if (VARIANT == 3) fe_mul_fast_v<1 - PCMM_MUL_PRODUCT>(x[c], x[c], y);
+#endif
             else fe_mul(x[c], x[c], y);
         }
     }
@@ -360,6 +363,7 @@ cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s) {
     if (variant == 1) k_bench_fp_mul<1><<<blocks, threads, 0, s>>>(iters, out);
     else if (variant == 2) k_bench_fp_mul<2><<<blocks, threads, 0, s>>>(iters, out);
+    else if (variant == 3) k_bench_fp_mul<3><<<blocks, threads, 0, s>>>(iters, out);
     else k_bench_fp_mul<0><<<blocks, threads, 0, s>>>(iters, out);
     return cudaGetLastError();
 }

@@ -4,7 +4,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2504_14497_b200 import pcmm as P
 
-for v, name in ((0, "fe_mul (default)"), (1, "fe_mul_portable"), (2, "fe_add")):
+for v, name in ((0, "fe_mul (default)"), (3, "fe_mul other prod"), (1, "fe_mul_portable"), (2, "fe_add")):
     for blocks in (148 * 4, 148 * 8):
         P.bench_fp_mul(v, blocks, 128, 16)
         s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
