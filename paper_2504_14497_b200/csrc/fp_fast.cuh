@@ -174,11 +174,8 @@ __device__ __forceinline__ void fe_prod_eo(uint32_t T[16], const fe &a, const fe
 #define PCMM_MUL_PRODUCT 1        // 1: even/odd product scanning, 0: operand scanning
 #endif
 
-template <int PV>
-__device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
-    uint32_t T[16];
-    if (PV == 1) fe_prod_eo(T, a, b);
-    else fe_prod_os(T, a, b);
+// Montgomery reduction of a 512-bit T (T < p 2^256) to T 2^-256 mod p in [0, p)
+__device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) {
     // ---- reduction, 64-bit quotient digits: -p^-1 = 1 mod 2^64 (p = -1 mod 2^96),
     // so round r (base b = 2r) takes q = T[b] + 2^32 T[b+1] and adds
     //   q p 2^(32b) = -q + q 2^96 + u 2^192,  u = q (2^64 - 2^32 + 1) < 2^128.
@@ -233,7 +230,127 @@ __device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
     for (int k = 0; k < 8; k++) r.v[k] = (T[8 + k] & m) | (t[k] & ~m);
 }
 
+template <int PV>
+__device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
+    uint32_t T[16];
+    if (PV == 1) fe_prod_eo(T, a, b);
+    else fe_prod_os(T, a, b);
+    fe_redc_fast(r, T);
+}
+
 __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) { fe_mul_fast_v<PCMM_MUL_PRODUCT>(r, a, b); }
+
+// ---- squaring: the 28 cross products a_i a_j (i < j) once, in the even/odd
+// accumulators (row i: j - i odd -> O, j - i even -> E; chains of 1..4 pairs),
+// C = E + O 2^32, T = 2 C + sum a_i^2 2^(64 i) (the diagonal as one fused
+// IMAD.WIDE.U32.X chain over all 16 words): 36 products instead of 64.
+#define PCMM_CH1C(d0, d1, c, x0, y)                                \
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"                       \
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"                      \
+        "addc.u32 %2, %2, 0;"                                      \
+        : "+r"(d0), "+r"(d1), "+r"(c)                              \
+        : "r"(x0), "r"(y))
+#define PCMM_CH2C(d0, d1, d2, d3, c, x0, x1, y)                    \
+    asm("mad.lo.cc.u32 %0, %5, %7, %0;\n\t"                       \
+        "madc.hi.cc.u32 %1, %5, %7, %1;\n\t"                      \
+        "madc.lo.cc.u32 %2, %6, %7, %2;\n\t"                      \
+        "madc.hi.cc.u32 %3, %6, %7, %3;\n\t"                      \
+        "addc.u32 %4, %4, 0;"                                      \
+        : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3), "+r"(c)          \
+        : "r"(x0), "r"(x1), "r"(y))
+#define PCMM_CH3C(d0, d1, d2, d3, d4, d5, c, x0, x1, x2, y)        \
+    asm("mad.lo.cc.u32 %0, %7, %10, %0;\n\t"                      \
+        "madc.hi.cc.u32 %1, %7, %10, %1;\n\t"                     \
+        "madc.lo.cc.u32 %2, %8, %10, %2;\n\t"                     \
+        "madc.hi.cc.u32 %3, %8, %10, %3;\n\t"                     \
+        "madc.lo.cc.u32 %4, %9, %10, %4;\n\t"                     \
+        "madc.hi.cc.u32 %5, %9, %10, %5;\n\t"                     \
+        "addc.u32 %6, %6, 0;"                                      \
+        : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3), "+r"(d4), "+r"(d5), "+r"(c) \
+        : "r"(x0), "r"(x1), "r"(x2), "r"(y))
+
+__device__ __forceinline__ void fe_sqr_fast(fe &r, const fe &a) {
+    const uint32_t a0 = a.v[0], a1 = a.v[1], a2 = a.v[2], a3 = a.v[3];
+    const uint32_t a4 = a.v[4], a5 = a.v[5], a6 = a.v[6], a7 = a.v[7];
+    uint32_t E[16], O[16];                       // E[k] = word k (k >= 2), O[k] = word k + 1
+    // row 0: plain products; O[0..7] = a0 (a1, a3, a5, a7), E[2..7] = a0 (a2, a4, a6)
+    {
+        uint64_t p;
+        p = (uint64_t)a0 * a1; O[0] = (uint32_t)p; O[1] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a3; O[2] = (uint32_t)p; O[3] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a5; O[4] = (uint32_t)p; O[5] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a7; O[6] = (uint32_t)p; O[7] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a2; E[2] = (uint32_t)p; E[3] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a4; E[4] = (uint32_t)p; E[5] = (uint32_t)(p >> 32);
+        p = (uint64_t)a0 * a6; E[6] = (uint32_t)p; E[7] = (uint32_t)(p >> 32);
+    }
+#pragma unroll
+    for (int k = 8; k < 16; k++) {
+        E[k] = 0;
+        O[k] = 0;
+    }
+    // row i: O-chain over j = i+1, i+3, .. at O[2i ..], E-chain over j = i+2, .. at E[2i+2 ..]
+    PCMM_CH3C(O[2], O[3], O[4], O[5], O[6], O[7], O[8], a2, a4, a6, a1);        // i = 1
+    PCMM_CH3C(E[4], E[5], E[6], E[7], E[8], E[9], E[10], a3, a5, a7, a1);
+    PCMM_CH3C(O[4], O[5], O[6], O[7], O[8], O[9], O[10], a3, a5, a7, a2);       // i = 2
+    PCMM_CH2C(E[6], E[7], E[8], E[9], E[10], a4, a6, a2);
+    PCMM_CH2C(O[6], O[7], O[8], O[9], O[10], a4, a6, a3);                       // i = 3
+    PCMM_CH2C(E[8], E[9], E[10], E[11], E[12], a5, a7, a3);
+    PCMM_CH2C(O[8], O[9], O[10], O[11], O[12], a5, a7, a4);                     // i = 4
+    PCMM_CH1C(E[10], E[11], E[12], a6, a4);
+    PCMM_CH1C(O[10], O[11], O[12], a6, a5);                                     // i = 5
+    PCMM_CH1C(E[12], E[13], E[14], a7, a5);
+    PCMM_CH1C(O[12], O[13], O[14], a7, a6);                                     // i = 6
+    // C = E + O 2^32 (C[0] = 0, C[1] = O[0]); C < 2^511
+    uint32_t C[16];
+    C[0] = 0;
+    C[1] = O[0];
+    asm("add.cc.u32 %0, %14, %28;\n\t"
+        "addc.cc.u32 %1, %15, %29;\n\t"
+        "addc.cc.u32 %2, %16, %30;\n\t"
+        "addc.cc.u32 %3, %17, %31;\n\t"
+        "addc.cc.u32 %4, %18, %32;\n\t"
+        "addc.cc.u32 %5, %19, %33;\n\t"
+        "addc.cc.u32 %6, %20, %34;\n\t"
+        "addc.cc.u32 %7, %21, %35;\n\t"
+        "addc.cc.u32 %8, %22, %36;\n\t"
+        "addc.cc.u32 %9, %23, %37;\n\t"
+        "addc.cc.u32 %10, %24, %38;\n\t"
+        "addc.cc.u32 %11, %25, %39;\n\t"
+        "addc.cc.u32 %12, %26, %40;\n\t"
+        "addc.u32 %13, %27, %41;"
+        : "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]), "=r"(C[8]), "=r"(C[9]),
+          "=r"(C[10]), "=r"(C[11]), "=r"(C[12]), "=r"(C[13]), "=r"(C[14]), "=r"(C[15])
+        : "r"(E[2]), "r"(E[3]), "r"(E[4]), "r"(E[5]), "r"(E[6]), "r"(E[7]), "r"(E[8]), "r"(E[9]), "r"(E[10]),
+          "r"(E[11]), "r"(E[12]), "r"(E[13]), "r"(E[14]), "r"(E[15]),
+          "r"(O[1]), "r"(O[2]), "r"(O[3]), "r"(O[4]), "r"(O[5]), "r"(O[6]), "r"(O[7]), "r"(O[8]), "r"(O[9]),
+          "r"(O[10]), "r"(O[11]), "r"(O[12]), "r"(O[13]), "r"(O[14]));
+    uint32_t T[16];
+    T[0] = 0;
+#pragma unroll
+    for (int k = 1; k < 16; k++) T[k] = __funnelshift_l(C[k - 1], C[k], 1);   // 2 C
+    asm("mad.lo.cc.u32 %0, %16, %16, %0;\n\t"
+        "madc.hi.cc.u32 %1, %16, %16, %1;\n\t"
+        "madc.lo.cc.u32 %2, %17, %17, %2;\n\t"
+        "madc.hi.cc.u32 %3, %17, %17, %3;\n\t"
+        "madc.lo.cc.u32 %4, %18, %18, %4;\n\t"
+        "madc.hi.cc.u32 %5, %18, %18, %5;\n\t"
+        "madc.lo.cc.u32 %6, %19, %19, %6;\n\t"
+        "madc.hi.cc.u32 %7, %19, %19, %7;\n\t"
+        "madc.lo.cc.u32 %8, %20, %20, %8;\n\t"
+        "madc.hi.cc.u32 %9, %20, %20, %9;\n\t"
+        "madc.lo.cc.u32 %10, %21, %21, %10;\n\t"
+        "madc.hi.cc.u32 %11, %21, %21, %11;\n\t"
+        "madc.lo.cc.u32 %12, %22, %22, %12;\n\t"
+        "madc.hi.cc.u32 %13, %22, %22, %13;\n\t"
+        "madc.lo.cc.u32 %14, %23, %23, %14;\n\t"
+        "madc.hi.u32 %15, %23, %23, %15;"
+        : "+r"(T[0]), "+r"(T[1]), "+r"(T[2]), "+r"(T[3]), "+r"(T[4]), "+r"(T[5]), "+r"(T[6]), "+r"(T[7]),
+          "+r"(T[8]), "+r"(T[9]), "+r"(T[10]), "+r"(T[11]), "+r"(T[12]), "+r"(T[13]), "+r"(T[14]), "+r"(T[15])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7));
+    fe_redc_fast(r, T);
+}
+
 
 // r = a + b mod p (a, b < p)
 __device__ __forceinline__ void fe_add_fast(fe &r, const fe &a, const fe &b) {
@@ -318,6 +435,14 @@ __device__ __noinline__ fe2 fe_mul2_call(const fe a0, const fe b0, const fe a1, 
     fe2 r;
     fe_mul_fast(r.x, a0, b0);
     fe_mul_fast(r.y, a1, b1);
+    return r;
+}
+
+// One product and one square in one out-of-line call: (a b, c^2).
+__device__ __noinline__ fe2 fe_mulsqr_call(const fe a, const fe b, const fe c) {
+    fe2 r;
+    fe_mul_fast(r.x, a, b);
+    fe_sqr_fast(r.y, c);
     return r;
 }
 

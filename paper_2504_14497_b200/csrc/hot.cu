@@ -79,13 +79,13 @@ __device__ __forceinline__ void jac_add_aff(jacc &A, const fe &x2, const fe &y2)
         A = jac_add_slow(A, x2, y2);
         return;
     }
-    fe S2, HH;
-    mul2(S2, y2, T1, HH, H, H);                   // S2 = y2 Z^3, HH = H^2
+    const fe2 sh = fe_mulsqr_call(y2, T1, H);     // S2 = y2 Z^3, HH = H^2
+    const fe &S2 = sh.x, &HH = sh.y;
     fe R;
     fe_sub(R, S2, A.Y);
     const fe3 t = fe_mul3_call(H, HH, A.X, HH, A.ZZ, HH);  // H^3, V = X1 H^2, ZZ3
-    fe R2, Z3;
-    mul2(R2, R, R, Z3, A.Z, H);                   // R^2, Z3 = Z1 H
+    const fe2 zr = fe_mulsqr_call(A.Z, H, R);     // Z3 = Z1 H, R^2
+    const fe &Z3 = zr.x, &R2 = zr.y;
     fe X3, V2, D;
     fe_add(V2, t.y, t.y);
     fe_sub(X3, R2, t.x);

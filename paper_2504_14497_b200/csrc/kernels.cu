@@ -670,6 +670,10 @@ __global__ void k_test_field(int op, const uint8_t *__restrict__ a, const uint8_
         case 1: fe_sub(r, x, y); break;
         case 2: fe_mul(r, x, y); break;
         case 3: fe_inv(r, x); break;
+#ifdef __CUDA_ARCH__
+        case 5: fe_sqr_fast(r, x); break;
+        case 6: fe_mul_fast_v<1 - PCMM_MUL_PRODUCT>(r, x, y); break;
+#endif
         default: fe_neg(r, x); break;
     }
     fe_from_mont(r, r);

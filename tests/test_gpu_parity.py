@@ -48,7 +48,8 @@ def test_field_ops_bit_exact():
     A = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in a), dtype=np.uint8).reshape(-1, 32))
     B = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in b), dtype=np.uint8).reshape(-1, 32))
     for op, f in [(0, lambda x, y: (x + y) % ecref.P), (1, lambda x, y: (x - y) % ecref.P),
-                  (2, lambda x, y: x * y % ecref.P), (4, lambda x, y: (-x) % ecref.P)]:
+                  (2, lambda x, y: x * y % ecref.P), (4, lambda x, y: (-x) % ecref.P),
+                  (5, lambda x, y: x * x % ecref.P), (6, lambda x, y: x * y % ecref.P)]:
         out = P.test_field(op, A, B).cpu().numpy()
         for i in range(len(a)):
             assert int.from_bytes(out[i].tobytes(), "big") == f(a[i], b[i]), (op, i)
