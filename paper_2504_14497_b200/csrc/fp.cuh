@@ -211,7 +211,13 @@ PCMM_HD void fe_neg(fe &r, const fe &a) {
     fe_sub(r, z, a);
 }
 
-PCMM_HD void fe_sqr(fe &r, const fe &a) { fe_mul(r, a, a); }
+PCMM_HD void fe_sqr(fe &r, const fe &a) {
+#if defined(__CUDA_ARCH__) && defined(PCMM_HAVE_FAST_MUL)
+    fe_sqr_fast(r, a);
+#else
+    fe_mul_portable(r, a, a);
+#endif
+}
 
 PCMM_HD void fe_to_mont(fe &r, const fe &a) {
     fe r2;

@@ -335,10 +335,9 @@ __global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ 
 // ------------------------------------------------------------ a3': tables -> affine
 // The accumulate loop adds table entries with the Jacobian + affine mixed
 // addition (hot.cu), so the tables are converted once to affine (x, y) =
-// (X/Z, Y/Z) with Montgomery's simultaneous inversion: each thread takes 2 x
-// `pairs` entries (stride = grid size, so a warp reads consecutive entries) as
-// two interleaved product chains (independent products: twice the ILP), one
-// fe_inv per thread, 5 products per entry.  The prefix products are parked in
+// (X/Z, Y/Z) with Montgomery's simultaneous inversion: each lane takes `batch`
+// entries (stride = grid size, so a warp reads consecutive entries), one fe_inv
+// per CTA (below), 5 products per entry.  The prefix products are parked in
 // the output's y words between the two passes.  Identity entries (Z = 0:
 // slot 0 and unused slots) become x = all ones (hot.cu aff_is_inf).
 struct AffIn {
@@ -399,44 +398,85 @@ __device__ __forceinline__ fe aff_prefix(const uint32_t *__restrict__ atab, int6
     return fe{{p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w}};
 }
 
-__global__ void __launch_bounds__(128) k_affine(const uint32_t *__restrict__ tab, int64_t entries, int pairs,
+__device__ __forceinline__ fe fe_shfl_up(const fe &a, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = __shfl_up_sync(0xffffffffu, a.v[i], d);
+    return r;
+}
+
+__device__ __forceinline__ fe fe_shfl_down(const fe &a, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], d);
+    return r;
+}
+
+// One inversion per CTA (128 lanes x `batch` entries): lane products -> warp
+// prefix/suffix products (shuffles) -> the four warp totals -> lane 0 of warp 0
+// inverts their product and hands each warp the inverse of its total; each lane
+// then recovers 1 / (its product) = inv(warp total) x (prefix before it) x
+// (suffix after it).  The other warps wait at the barrier while other CTAs run.
+__global__ void __launch_bounds__(128) k_affine(const uint32_t *__restrict__ tab, int64_t entries, int batch,
                                                uint32_t *__restrict__ atab) {
+    __shared__ fe wtot[4], winv[4];
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= entries) return;
-    fe acc0, acc1;
-    fe_one_mont(acc0);
-    acc1 = acc0;
-    for (int r = 0; r < pairs; r++) {             // chain 0: entries t + 2rT, chain 1: t + (2r+1)T
-        const int64_t e0 = t + (2 * r) * T, e1 = e0 + T;
-        if (e0 >= entries) break;
-        const AffIn a0 = aff_load_z(tab, e0, entries), a1 = aff_load_z(tab, e1, entries);
-        aff_pass1_store(atab, e0, entries, a0, acc0);
-        aff_pass1_store(atab, e1, entries, a1, acc1);
-        fe n0, n1;
-        fe_mul(n0, acc0, a0.z);
-        fe_mul(n1, acc1, a1.z);
-        acc0 = n0;
-        acc1 = n1;
+    const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+    fe one;
+    fe_one_mont(one);
+    fe acc = one;
+    for (int r = 0; r < batch; r++) {
+        const int64_t e = t + r * T;
+        if (e >= entries) break;
+        const AffIn a0 = aff_load_z(tab, e, entries);
+        aff_pass1_store(atab, e, entries, a0, acc);
+        if (a0.ok) fe_mul(acc, acc, a0.z);
     }
-    fe tot, inv, inv0, inv1;
-    fe_mul(tot, acc0, acc1);
-    fe_inv(inv, tot);
-    fe_mul(inv0, inv, acc1);                      // 1 / acc0
-    fe_mul(inv1, inv, acc0);                      // 1 / acc1
-    for (int r = pairs - 1; r >= 0; r--) {
-        const int64_t e0 = t + (2 * r) * T, e1 = e0 + T;
-        if (e0 >= entries) continue;
-        const AffIn a0 = aff_load_z(tab, e0, entries), a1 = aff_load_z(tab, e1, entries);
-        fe zi0, zi1, n0, n1;
-        if (a0.ok) fe_mul(zi0, inv0, aff_prefix(atab, e0));
-        if (a1.ok) fe_mul(zi1, inv1, aff_prefix(atab, e1));
-        fe_mul(n0, inv0, a0.z);
-        fe_mul(n1, inv1, a1.z);
-        inv0 = n0;
-        inv1 = n1;
-        if (a0.ok) aff_pass2_store(tab, atab, e0, zi0);
-        if (a1.ok) aff_pass2_store(tab, atab, e1, zi1);
+    // warp-inclusive prefix (Q) and suffix (S) products of the lane products
+    fe Q = acc, S = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const fe q = fe_shfl_up(Q, d), sv = fe_shfl_down(S, d);
+        fe qm, sm;
+        fe_mul(qm, Q, q);
+        fe_mul(sm, S, sv);
+        if (lane >= d) Q = qm;
+        if (lane + d < 32) S = sm;
+    }
+    if (lane == 31) wtot[warp] = Q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fe p1 = wtot[0], p2, p3, tot, s2, s1, inv, x;
+        fe_mul(p2, p1, wtot[1]);
+        fe_mul(p3, p2, wtot[2]);
+        fe_mul(tot, p3, wtot[3]);
+        fe_mul(s2, wtot[2], wtot[3]);
+        fe_mul(s1, wtot[1], s2);
+        fe_inv(inv, tot);
+        fe_mul(winv[0], inv, s1);                  // 1 / W0
+        fe_mul(x, inv, p1);
+        fe_mul(winv[1], x, s2);                    // 1 / W1
+        fe_mul(x, inv, p2);
+        fe_mul(winv[2], x, wtot[3]);               // 1 / W2
+        fe_mul(winv[3], inv, p3);                  // 1 / W3
+    }
+    __syncthreads();
+    fe qprev = fe_shfl_up(Q, 1), snext = fe_shfl_down(S, 1);
+    if (lane == 0) qprev = one;
+    if (lane == 31) snext = one;
+    fe inv;
+    fe_mul(inv, winv[warp], qprev);
+    fe_mul(inv, inv, snext);                       // 1 / acc (this lane's product)
+    for (int r = batch - 1; r >= 0; r--) {
+        const int64_t e = t + r * T;
+        if (e >= entries) continue;
+        const AffIn a0 = aff_load_z(tab, e, entries);
+        if (!a0.ok) continue;
+        fe zi;
+        fe_mul(zi, inv, aff_prefix(atab, e));      // 1 / Z_e
+        fe_mul(inv, inv, a0.z);                    // 1 / (product of this lane's Z before e)
+        aff_pass2_store(tab, atab, e, zi);
     }
 }
 
@@ -729,17 +769,17 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
 
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s) {
     if (entries <= 0) return cudaSuccess;
-    // up to 2 x 32 entries per thread (the inversion amortised over 64), but at
-    // least one CTA per SM (measured at 256^3: 32 pairs 0.47 ms, 16 0.51, 8 0.65)
-    static int pairs_env = -1;
-    if (pairs_env < 0) {
-        const char *e = getenv("PCMM_AFFINE_PAIRS");
-        pairs_env = e ? atoi(e) : 0;
+    // up to 32 entries per lane (one inversion per 4096 entries), fewer when that
+    // would leave fewer than ~4 warps per SM (256^3: batch 32 0.48 ms, 16 0.55, 8 0.76)
+    static int batch_env = -1;
+    if (batch_env < 0) {
+        const char *e = getenv("PCMM_AFFINE_BATCH");
+        batch_env = e ? atoi(e) : 0;
     }
     const int64_t want = (int64_t)num_sms() * 128;
-    int pairs = pairs_env > 0 ? pairs_env : (int)std::min<int64_t>(32, std::max<int64_t>(1, entries / (2 * want)));
-    const int64_t threads = (entries + 2 * pairs - 1) / (2 * pairs);
-    k_affine<<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, pairs, atables);
+    const int batch = batch_env > 0 ? batch_env : (int)std::min<int64_t>(32, std::max<int64_t>(1, entries / want));
+    const int64_t threads = (entries + batch - 1) / batch;
+    k_affine<<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables);
     return cudaGetLastError();
 }
 
