@@ -63,7 +63,7 @@ def lib():
             L.oracle_generator.argtypes = [u8p]
             L.oracle_pubkey.argtypes = [u8p, u8p]
             L.oracle_encrypt.argtypes = [u8p, ctypes.c_int64, i64p, u8p, u8p, ctypes.c_int]
-            L.oracle_closed_form.argtypes = [u8p, ctypes.c_int, ctypes.POINTER(ctypes.c_int16), i64p, u8p, u8p]
+            L.oracle_closed_form.argtypes = [u8p, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), i64p, u8p, u8p]
             L.oracle_decrypt.argtypes = [u8p, ctypes.c_int64, u8p, ctypes.c_int64, ctypes.c_int64, i64p,
                                          ctypes.POINTER(ctypes.c_int32)]
             L.oracle_cussen_counts.argtypes = [i64p, ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(ctypes.c_int)]
@@ -72,9 +72,9 @@ def lib():
             L.oracle_cussen_vs_mul_plain.argtypes = [i64p, ctypes.c_int, ctypes.c_int64, ctypes.c_int, i64p]
             L.oracle_cussen_vs_mul_encrypted.argtypes = [i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p,
                                                          u64p]
-            L.oracle_pcmm.argtypes = [ctypes.c_int] * 6 + [ctypes.POINTER(ctypes.c_int16), u8p, u8p, ctypes.c_int,
+            L.oracle_pcmm.argtypes = [ctypes.c_int] * 6 + [ctypes.POINTER(ctypes.c_int32), u8p, u8p, ctypes.c_int,
                                                           u64p]
-            L.oracle_inner_product.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int16), u8p, u8p]
+            L.oracle_inner_product.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int32), u8p, u8p]
             L.oracle_init()
             _lib = L
     return _lib
@@ -183,11 +183,11 @@ def encrypt(H: bytes, b: np.ndarray, r_be: np.ndarray, threads: int | None = Non
 
 def closed_form(x: int, a_row, b_col, r_col_be) -> bytes:
     """Eq. 5: Enc(sum a_k b_k) = (R G, (x R + c) G), R = sum a_k r_k mod q."""
-    a = np.ascontiguousarray(np.asarray(a_row).astype(np.int16)).reshape(-1)
+    a = np.ascontiguousarray(np.asarray(a_row).astype(np.int32)).reshape(-1)
     b = np.ascontiguousarray(b_col, dtype=np.int64).reshape(-1)
     r = np.ascontiguousarray(r_col_be, dtype=np.uint8).reshape(a.size, 32)
     out = _buf(128)
-    _check(lib().oracle_closed_form(_p(_b32(x)), a.size, _p(a, ctypes.c_int16), _p(b, ctypes.c_int64), _p(r),
+    _check(lib().oracle_closed_form(_p(_b32(x)), a.size, _p(a, ctypes.c_int32), _p(b, ctypes.c_int64), _p(r),
                                     _p(out)), "closed_form")
     return out.tobytes()
 
@@ -252,25 +252,25 @@ SCHOOLBOOK, CUSSEN = 0, 1
 
 
 def pcmm(path: int, A: np.ndarray, ct: np.ndarray, l: int, t: int, N: int = 4, threads: int | None = None):
-    """A: integer [m, n] (int8 / uint8 / wider, |a| < 2^15); ct: uint8 [n*l, 128] canonical, (k, j) row-major.
+    """A: integer [m, n] (int8 / uint8 / wider, |a| < 2^31); ct: uint8 [n*l, 128] canonical, (k, j) row-major.
     -> (out uint8 [m*l, 128], (adds, dbls, ecsm, ecsm_bits))."""
-    A = np.ascontiguousarray(np.asarray(A).astype(np.int16))
+    A = np.ascontiguousarray(np.asarray(A).astype(np.int32))
     m, n = A.shape
     ct = np.ascontiguousarray(ct, dtype=np.uint8).reshape(n * l, 128)
     out = np.zeros((m * l, 128), dtype=np.uint8)
     cnt = np.zeros(4, dtype=np.uint64)
     th = threads if threads else (os.cpu_count() or 1)
-    _check(lib().oracle_pcmm(path, m, n, l, t, N, _p(A, ctypes.c_int16), _p(ct), _p(out), th,
+    _check(lib().oracle_pcmm(path, m, n, l, t, N, _p(A, ctypes.c_int32), _p(ct), _p(out), th,
                              _p(cnt, ctypes.c_uint64)), "pcmm")
     return out, tuple(int(x) for x in cnt)
 
 
 def inner_product(a_row: np.ndarray, ct_col: np.ndarray) -> bytes:
     """Enc(sum_k a_k b_k) from a row of A and a column of n ciphertexts (definition)."""
-    a = np.ascontiguousarray(np.asarray(a_row).astype(np.int16)).reshape(-1)
+    a = np.ascontiguousarray(np.asarray(a_row).astype(np.int32)).reshape(-1)
     c = np.ascontiguousarray(ct_col, dtype=np.uint8).reshape(a.size, 128)
     out = _buf(128)
-    _check(lib().oracle_inner_product(a.size, _p(a, ctypes.c_int16), _p(c), _p(out)), "inner_product")
+    _check(lib().oracle_inner_product(a.size, _p(a, ctypes.c_int32), _p(c), _p(out)), "inner_product")
     return out.tobytes()
 
 

@@ -535,8 +535,8 @@ EXPORT int oracle_encrypt(const uint8_t *H64, int64_t count, const int64_t *b, c
 /* Eq. 5 closed form of one output of PC-MM, straight from the
  * plaintext inputs: with R = sum_k a_k r_k mod q and c = sum_k a_k b_k,
  *   Enc(c) = ( R G , (x R + c) G ).
- * Inputs: x (32 B BE), a[n] (int8), b[n] (int64), r[n] (32 B BE each).         */
-EXPORT int oracle_closed_form(const uint8_t *x_be, int n, const int16_t *a, const int64_t *b, const uint8_t *r_be,
+ * Inputs: x (32 B BE), a[n] (int32), b[n] (int64), r[n] (32 B BE each).         */
+EXPORT int oracle_closed_form(const uint8_t *x_be, int n, const int32_t *a, const int64_t *b, const uint8_t *r_be,
                               uint8_t *out128) {
     oracle_init_once();
     big R = big_u64(0), c = big_u64(0);
@@ -754,7 +754,7 @@ EXPORT int oracle_cussen_vs_mul_encrypted(const int64_t *a, int len, int t, int 
 /* ================================================ PC-MM engines ============ */
 typedef struct {
     int m, n, l, t, N, path;
-    const int16_t *A;
+    const int32_t *A;
     const jac *B;              /* [n*l*2] parsed ciphertext points, (k, j, c) */
     const colplan *plans;      /* [n] (Cussen) */
     uint8_t *out;              /* [m*l*128] */
@@ -813,7 +813,7 @@ static void *cussen_worker(void *arg) {
  * width, cost model).  N: Cussen iterations (the paper uses 4).  ct: n*l
  * canonical ciphertexts (k, j) row-major.  out: m*l canonical ciphertexts.
  * cnt_out[4] = executed adds, doublings, ECSMs, ECSM bits.                    */
-EXPORT int oracle_pcmm(int path, int m, int n, int l, int t, int N, const int16_t *A, const uint8_t *ct,
+EXPORT int oracle_pcmm(int path, int m, int n, int l, int t, int N, const int32_t *A, const uint8_t *ct,
                        uint8_t *out, int nthreads, uint64_t *cnt_out) {
     oracle_init_once();
     if (m <= 0 || n <= 0 || l <= 0) return -2;
@@ -855,7 +855,7 @@ EXPORT int oracle_pcmm(int path, int m, int n, int l, int t, int N, const int16_
 
 /* One output ciphertext C_ij of the schoolbook definition (for sampled parity
  * at full sizes): row a[0..n-1] against the column ct[k] (n canonical cts).    */
-EXPORT int oracle_inner_product(int n, const int16_t *a, const uint8_t *ct_col, uint8_t *out128) {
+EXPORT int oracle_inner_product(int n, const int32_t *a, const uint8_t *ct_col, uint8_t *out128) {
     oracle_init_once();
     jac acc[2] = {jac_inf(), jac_inf()};
     for (int k = 0; k < n; k++)

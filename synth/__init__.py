@@ -149,7 +149,10 @@ def make_instance(cfg: Config, m: int | None = None, n: int | None = None, l: in
     g = SplitMix64(seed)
     x = g.scalar256()
     lo, hi = cfg.a_range
-    A = g.small(lo, hi, m * n).reshape(m, n).astype(np.int8 if cfg.signed else np.uint8)
+    # w <= 8: one byte per entry (int8 signed / uint8 unsigned, the pcmm_mul_* ABI);
+    # w > 8 (the paper's t = 12, 16 grid): int32 (the pcmm_mul_*_wide ABI)
+    dt = (np.int8 if cfg.signed else np.uint8) if cfg.w <= 8 else np.int32
+    A = g.small(lo, hi, m * n).reshape(m, n).astype(dt)
     B = g.small(cfg.b_lo, cfg.b_hi, n * l).reshape(n, l).astype(np.int32)
     r = g.scalars256(n * l)
     c = Config(cfg.name, m, n, l, cfg.w, cfg.signed, cfg.b_lo, cfg.b_hi, seed)

@@ -74,3 +74,28 @@ def test_c64_cussen_equals_schoolbook_p5():
     for (i, j) in [(0, 0), (17, 42), (63, 63)]:
         assert oc[i * 64 + j].tobytes() == _closed(I, i, j)
     assert oracle.inner_product(I.A[17], ct.reshape(64, 64, 128)[:, 42]) == oc[17 * 64 + 42].tobytes()
+
+
+@pytest.mark.parametrize("t,signed", [(12, False), (16, False), (16, True)])
+def test_wide_plaintexts_t12_t16(t, signed):
+    # the paper's t = 12, 16 grid (Table A9): plaintexts wider than a byte, unsigned
+    # 16-bit values above 2^15 included; Cussen == schoolbook == Eq. 5 closed form
+    cfg = synth.Config(f"w{t}", 6, 7, 3, t, signed, 0, 255, 41 + t)
+    I = synth.make_instance(cfg)
+    assert I.A.dtype == np.int32
+    A = I.A.copy()
+    if not signed:
+        A[0, 0], A[1, 0], A[2, 1] = (1 << t) - 1, (1 << t) - 2, 1 << (t - 1)
+    else:
+        A[0, 0], A[1, 0] = -(1 << (t - 1)), (1 << (t - 1)) - 1
+    ct = _encrypt(I)
+    oc, _ = oracle.pcmm(oracle.CUSSEN, A, ct, 3, t)
+    os_, _ = oracle.pcmm(oracle.SCHOOLBOOK, A, ct, 3, t)
+    assert (oc == os_).all()
+    n = 7
+    for i in range(6):
+        for j in range(3):
+            r = [int.from_bytes(I.r_be[k * 3 + j].tobytes(), "big") for k in range(n)]
+            R = sum(int(A[i, k]) * r[k] for k in range(n))
+            c = sum(int(A[i, k]) * int(I.B[k, j]) for k in range(n))
+            assert oc[i * 3 + j].tobytes() == ecref.enc_closed_form(I.x, R, c)
