@@ -142,6 +142,28 @@ PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int 
 PCMM_API int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int leaf,
                                const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
 
+/* Wide-plaintext PC-MM (the paper's t = 12, 16 grid,
+ * PAPER.md:61, Table A9): the same products as pcmm_mul_schoolbook /
+ * pcmm_mul_cussen for plaintexts of up to 16 bits.
+ *   A_d : int32[m][n] row-major (4-byte aligned); entries in [0, 2^w)
+ *         (unsigned) or [-2^(w-1), 2^(w-1)) (is_signed), w in [1, 16];
+ *         m <= 16384 (a column is sorted in shared memory).
+ * Cussen (Alg. 3): per column up to min(m, 2^w - 1) distinct values, so the
+ * compression plan, the uint16 rank and the tables (min(m, 2^w - 1) + 1 slots
+ * per (k, j, c)) are sized per problem; the tables are built, converted to
+ * affine and accumulated in chunks of inner indices k chosen so that one
+ * chunk's tables fit a 2 GiB budget (env PCMM_WIDE_BUDGET_MB overrides).
+ * Output, status and errors as pcmm_mul_cussen / pcmm_mul_schoolbook, with
+ * the workspace sized by pcmm_workspace_bytes_wide (path 0 schoolbook,
+ * 1 Cussen; returns 0 for invalid arguments).  Async.                      */
+PCMM_API size_t pcmm_workspace_bytes_wide(int m, int n, int l, int w, int path);
+PCMM_API int pcmm_mul_cussen_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, int iters,
+                                  const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes,
+                                  void *stream);
+PCMM_API int pcmm_mul_schoolbook_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed,
+                                      const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes,
+                                      void *stream);
+
 /* Normalise `count` projective ciphertexts (layout above, as written by
  * pcmm_mul_*) to canonical affine bytes ctC_d[count][128] (x = X/Z, y = Y/Z,
  * out of Montgomery form, big-endian; infinity -> 64 zero bytes), by

@@ -102,6 +102,50 @@ Layout layout(int m, int n, int l, int w, int path) {
     return L;
 }
 
+// ---------------------------------------------------------------- wide-plaintext workspace
+struct LayoutW {
+    size_t bsoa = 0, pn = 0, psN = 0, pptr = 0, rank = 0, tables = 0, scratch = 0, total = 0;
+    int cap = 0, S = 0, KC = 0;
+};
+
+constexpr int kWideMaxM = 16384;        // k_plan_wide sorts a column in shared memory
+
+LayoutW layout_wide(int m, int n, int l, int w, int path) {
+    LayoutW L;
+    size_t off = 256;
+    const size_t cnt = (size_t)n * l;
+    L.bsoa = off;
+    off = align256(off + cnt * 2 * kPtWords * 4);
+    if (path == PCMM_PATH_CUSSEN) {
+        L.cap = (int)std::min<int64_t>(m, (1LL << w) - 1);
+        L.S = L.cap + 1;
+        // chunk of inner indices k whose tables (+ scratch / affine tables) fit the budget
+        size_t budget = (size_t)2 << 30;
+        if (const char *e = getenv("PCMM_WIDE_BUDGET_MB")) budget = (size_t)atoll(e) << 20;
+        const size_t per_k = 2 * (size_t)l *
+                             ((size_t)L.S * kPtWords * 4 +
+                              std::max((size_t)2 * L.cap * kPtWords * 4, (size_t)L.S * kAffWords * 4));
+        int kc = (int)std::max<size_t>(1, std::min<size_t>((size_t)n, budget / per_k));
+        const int chunks = (n + kc - 1) / kc;
+        L.KC = (n + chunks - 1) / chunks;
+        L.pn = off;
+        off = align256(off + (size_t)n * 4 * 4);
+        L.psN = off;
+        off = align256(off + (size_t)n * L.cap * 4);
+        L.pptr = off;
+        off = align256(off + (size_t)n * 3 * L.cap * 2);
+        L.rank = off;
+        off = align256(off + (size_t)n * m * 2);
+        L.tables = off;
+        off = align256(off + (size_t)L.KC * 2 * l * L.S * kPtWords * 4);
+        L.scratch = off;
+        off = align256(off + (size_t)L.KC * 2 * l *
+                                 std::max((size_t)2 * L.cap * kPtWords * 4, (size_t)L.S * kAffWords * 4));
+    }
+    L.total = off;
+    return L;
+}
+
 int check_dims(int m, int n, int l) {
     if (m <= 0 || n <= 0 || l <= 0) return fail(PCMM_EDIM, "dimensions must be positive");
     if ((int64_t)m * l > (1LL << 30) || (int64_t)n * l > (1LL << 30) || (int64_t)m * n > (1LL << 31))
@@ -296,6 +340,61 @@ int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed
                     void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
     return mul_common(PCMM_PATH_CUSSEN, A_d, m, n, l, w, is_signed, iters, ctB_d, ctC_proj_d, ws_d, ws_bytes,
                       (cudaStream_t)stream);
+}
+
+size_t pcmm_workspace_bytes_wide(int m, int n, int l, int w, int path) {
+    if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 16 || m > kWideMaxM) return 0;
+    if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN) return 0;
+    return layout_wide(m, n, l, w, path).total;
+}
+
+static int mul_wide(int path, const int32_t *A_d, int m, int n, int l, int w, int is_signed, int iters,
+                    const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, cudaStream_t s) {
+    g_err.clear();
+    int rc = check_dims(m, n, l);
+    if (rc) return rc;
+    if (m > kWideMaxM) return fail(PCMM_EDIM, "wide path: m must be <= 16384");
+    if (!A_d || !ctB_d || !ctC_proj_d || !ws_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)A_d & 3) || ((uintptr_t)ctB_d & 15) || ((uintptr_t)ws_d & 255) || ((uintptr_t)ctC_proj_d & 15))
+        return fail(PCMM_EINVAL, "misaligned buffer (A 4 B, ctB/ctC 16 B, workspace 256 B)");
+    if (w < 1 || w > 16) return fail(PCMM_EINVAL, "w must be in [1, 16]");
+    if (path == PCMM_PATH_CUSSEN && (iters < 1 || iters > 4)) return fail(PCMM_ENOTSUP, "iters must be in [1, 4]");
+    const LayoutW L = layout_wide(m, n, l, w, path);
+    if (ws_bytes < L.total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_workspace_bytes_wide)");
+    uint8_t *ws = (uint8_t *)ws_d;
+    int *status = (int *)ws;
+    uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
+    uint32_t *out = (uint32_t *)ctC_proj_d;
+    CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
+    LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
+    if (path == PCMM_PATH_SCHOOLBOOK) {
+        LAUNCH("schoolbook", s, launch_schoolbook_wide(A_d, m, n, l, w, is_signed, bsoa, out, status, s));
+        return PCMM_OK;
+    }
+    int32_t *pn = (int32_t *)(ws + L.pn), *psN = (int32_t *)(ws + L.psN);
+    uint16_t *pptr = (uint16_t *)(ws + L.pptr), *rank = (uint16_t *)(ws + L.rank);
+    uint32_t *tables = (uint32_t *)(ws + L.tables), *scratch = (uint32_t *)(ws + L.scratch);
+    LAUNCH("plan", s, launch_plan_wide(A_d, m, n, w, is_signed, iters, L.cap, pn, psN, pptr, rank, status, s));
+    for (int k0 = 0; k0 < n; k0 += L.KC) {
+        const int kc = std::min(L.KC, n - k0);
+        LAUNCH("tables", s, launch_tables_wide(bsoa, pn, psN, pptr, n, l, iters, L.cap, L.S, k0, kc, tables, scratch,
+                                               s));
+        LAUNCH("affine", s, launch_affine(tables, 2LL * kc * l * L.S, scratch, s));
+        LAUNCH("accum", s, launch_accum_wide(scratch, rank, m, l, L.S, k0, kc, k0 == 0, out, s));
+    }
+    return PCMM_OK;
+}
+
+int pcmm_mul_cussen_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, int iters,
+                         const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_wide(PCMM_PATH_CUSSEN, A_d, m, n, l, w, is_signed, iters, ctB_d, ctC_proj_d, ws_d, ws_bytes,
+                    (cudaStream_t)stream);
+}
+
+int pcmm_mul_schoolbook_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, const uint8_t *ctB_d,
+                             void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_wide(PCMM_PATH_SCHOOLBOOK, A_d, m, n, l, w, is_signed, 0, ctB_d, ctC_proj_d, ws_d, ws_bytes,
+                    (cudaStream_t)stream);
 }
 
 int pcmm_normalize(const void *ctC_proj_d, int64_t count, uint8_t *ctC_d, void *ws_d, size_t ws_bytes, void *stream) {

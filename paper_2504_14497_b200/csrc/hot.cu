@@ -268,6 +268,74 @@ __global__ void __launch_bounds__(kRowsG, 3)
     soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
 }
 
+// ------------------------------------------------------------ a4 (wide path, NEXT-1): one k-chunk
+// As k_accum_g for the chunk k0 .. k0+kc-1 of the wide path (wide.cu): uint16
+// rank, tables [c][kk][j][slot][16].  The accumulator starts from the running
+// output (homogeneous (X : Y : Z) -> Jacobian (X Z, Y Z^2, Z)) unless this is
+// the first chunk, and the chunk's sum is written back to it.
+__global__ void __launch_bounds__(kRowsG, 3)
+    k_accum_gw(const uint32_t *__restrict__ tables, const uint16_t *__restrict__ rank, int m, int l, int S, int k0,
+               int kc, int first, uint32_t *__restrict__ out) {
+    int b = blockIdx.x;
+    const int j = b % l; b /= l;
+    const int c = b & 1; b >>= 1;
+    const int i = b * kRowsG + (int)threadIdx.x;
+    if (i >= m) return;
+    const int64_t cnt = (int64_t)m * l;
+    uint32_t *ob = out + (int64_t)c * kPtWords * cnt;
+    const int64_t oi = (int64_t)i * l + j;
+    jacc acc;
+    jac_init(acc);
+#ifdef __CUDA_ARCH__
+    if (!first) {
+        pt o;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            o.X.v[q] = ob[(0 * 8 + q) * cnt + oi];
+            o.Y.v[q] = ob[(1 * 8 + q) * cnt + oi];
+            o.Z.v[q] = ob[(2 * 8 + q) * cnt + oi];
+        }
+        if (!fe_is_zero(o.Z)) {
+            acc.Z = o.Z;
+            acc.ZZ = fe_mul_call(o.Z, o.Z);
+            mul2(acc.X, o.X, o.Z, acc.Y, o.Y, acc.ZZ);
+            acc.inf = 0;
+        }
+    }
+#endif
+    const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive kk
+    const uint32_t *tb = tables + (((int64_t)c * kc) * l + j) * (int64_t)S * kAffWords;
+    const uint16_t *rk = rank + (int64_t)k0 * m + i;
+    int k = 0;
+    while (k < kc && rk[(int64_t)k * m] == 0) k++;
+    if (k < kc) {
+        fe x2, y2;
+        load_aff(x2, y2, tb + k * tstride + (int64_t)rk[(int64_t)k * m] * kAffWords);
+        while (true) {
+            int kn = k + 1;
+            while (kn < kc && rk[(int64_t)kn * m] == 0) kn++;
+            fe xn, yn;
+            if (kn < kc) load_aff(xn, yn, tb + kn * tstride + (int64_t)rk[(int64_t)kn * m] * kAffWords);
+            jac_add_aff(acc, x2, y2);
+            if (kn >= kc) break;
+            x2 = xn;
+            y2 = yn;
+            k = kn;
+        }
+    }
+    pt o;
+    jac_to_proj(o, acc);
+    soa_store_hot(ob, cnt, oi, o);
+}
+
+cudaError_t launch_accum_wide(const uint32_t *atables, const uint16_t *rank, int m, int l, int S, int k0, int kc,
+                              int first, uint32_t *out, cudaStream_t s) {
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks);
+    k_accum_gw<<<grid, kRowsG, 0, s>>>(atables, rank, m, l, S, k0, kc, first, out);
+    return cudaGetLastError();
+}
+
 int accum_global_ctas_per_sm() {
     static int occ = 0;
     if (!occ) {

@@ -73,6 +73,18 @@ int num_sms();
 cudaError_t run_strassen(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa, int leaf,
                          uint32_t *out, int *status, cudaStream_t s);
 int accum_ctas_per_sm(int slots);
+// wide-plaintext path (wide.cu, hot.cu k_accum_gw): t <= 16, int32 A, uint16 rank, k-chunked tables
+int wide_plan_p2(int m);
+size_t wide_plan_smem(int m, int cap);
+cudaError_t launch_plan_wide(const int32_t *A, int m, int n, int w, int is_signed, int N, int cap, int32_t *pn,
+                             int32_t *psN, uint16_t *pptr, uint16_t *rank, int *status, cudaStream_t s);
+cudaError_t launch_tables_wide(const uint32_t *bsoa, const int32_t *pn, const int32_t *psN, const uint16_t *pptr,
+                               int n, int l, int N, int cap, int S, int k0, int kc, uint32_t *tables,
+                               uint32_t *scratch, cudaStream_t s);
+cudaError_t launch_accum_wide(const uint32_t *atables, const uint16_t *rank, int m, int l, int S, int k0, int kc,
+                              int first, uint32_t *out, cudaStream_t s);
+cudaError_t launch_schoolbook_wide(const int32_t *A, int m, int n, int l, int w, int is_signed,
+                                   const uint32_t *bsoa, uint32_t *out, int *status, cudaStream_t s);
 int accum_rows();
 
 }  // namespace pcmm

@@ -32,7 +32,7 @@ EXPORTS = [
     "pcmm_last_error", "pcmm_version", "pcmm_proj_bytes", "pcmm_keygen", "pcmm_encrypt", "pcmm_workspace_bytes",
     "pcmm_mul_schoolbook", "pcmm_mul_cussen", "pcmm_mul_strassen", "pcmm_normalize", "pcmm_decrypt_small", "pcmm_status",
     "pcmm_profile_enable", "pcmm_profile_read", "pcmm_test_field", "pcmm_test_point", "pcmm_test_plan",
-    "pcmm_bench_fp_mul",
+    "pcmm_bench_fp_mul", "pcmm_workspace_bytes_wide", "pcmm_mul_cussen_wide", "pcmm_mul_schoolbook_wide",
 ]
 
 
@@ -81,6 +81,10 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
             L.pcmm_test_point.argtypes = [i32, vp, vp, vp, vp, i64, vp]
             L.pcmm_test_plan.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp]
             L.pcmm_bench_fp_mul.argtypes = [i32, i32, i32, i32, vp, vp]
+            L.pcmm_workspace_bytes_wide.restype = sz
+            L.pcmm_workspace_bytes_wide.argtypes = [i32] * 5
+            L.pcmm_mul_cussen_wide.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+            L.pcmm_mul_schoolbook_wide.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             _lib = L
     return _lib
 
@@ -152,7 +156,10 @@ def decrypt_small(sk: bytes, ct: torch.Tensor, lo: int, hi: int, stream=None):
 
 
 # ------------------------------------------------------------------ PC-MM
-def workspace_bytes(m: int, n: int, l: int, w: int, path: int) -> int:
+def workspace_bytes(m: int, n: int, l: int, w: int, path: int, wide: bool = False) -> int:
+    """Workspace of pcmm_mul_* (wide=False: int8 / uint8 A, w <= 8) or pcmm_mul_*_wide (int32 A, w <= 16)."""
+    if wide:
+        return int(load().pcmm_workspace_bytes_wide(m, n, l, w, path))
     return int(load().pcmm_workspace_bytes(m, n, l, w, path))
 
 
@@ -160,8 +167,8 @@ def proj_bytes(count: int) -> int:
     return int(load().pcmm_proj_bytes(count))
 
 
-def alloc_workspace(m: int, n: int, l: int, w: int, path: int, device="cuda") -> torch.Tensor:
-    nb = workspace_bytes(m, n, l, w, path)
+def alloc_workspace(m: int, n: int, l: int, w: int, path: int, device="cuda", wide: bool = False) -> torch.Tensor:
+    nb = workspace_bytes(m, n, l, w, path, wide)
     if nb == 0:
         raise PCMMError(PCMM_EINVAL, "invalid dimensions for workspace")
     return torch.empty(nb, dtype=torch.uint8, device=device)   # caching allocator: 512 B aligned
@@ -177,6 +184,21 @@ def _mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signe
         raise PCMMError(PCMM_EDIM, "ctB must hold n*l canonical ciphertexts")
     if out_proj is None:
         out_proj = torch.empty(proj_bytes(m * l), dtype=torch.uint8, device=A.device)
+    if A.dtype == torch.int32:                     # wide plaintexts (w <= 16): pcmm_mul_*_wide
+        if path == STRASSEN:
+            raise PCMMError(PCMM_ENOTSUP, "Strassen takes int8 / uint8 plaintexts only")
+        if ws is None:
+            ws = alloc_workspace(m, n, l, w, path, A.device, wide=True)
+        L = load()
+        a = (_dev(A, torch.int32, "A"), m, n, l, w, int(bool(is_signed)))
+        if path == SCHOOLBOOK:
+            rc = L.pcmm_mul_schoolbook_wide(*a, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
+                                            ws.numel(), _stream(stream))
+        else:
+            rc = L.pcmm_mul_cussen_wide(*a, iters, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), _stream(stream))
+        _check(rc)
+        return out_proj, ws
     if ws is None:
         ws = alloc_workspace(m, n, l, w, path, A.device)
     # A's bytes are read as int8 (is_signed) or uint8 (unsigned, w up to 8)

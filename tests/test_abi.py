@@ -55,6 +55,9 @@ def test_validation_without_gpu():
     assert L.pcmm_workspace_bytes(0, 4, 4, 4, 1) == 0
     assert L.pcmm_workspace_bytes(4, 4, 4, 9, 1) == 0
     assert L.pcmm_workspace_bytes(4, 4, 4, 4, 1) > 0
+    assert L.pcmm_workspace_bytes_wide(4, 4, 4, 16, 1) > 0
+    assert L.pcmm_workspace_bytes_wide(4, 4, 4, 17, 1) == 0
+    assert L.pcmm_workspace_bytes_wide(16385, 4, 4, 16, 1) == 0
     rc = L.pcmm_mul_cussen(None, 0, 4, 4, 4, 0, 4, None, None, None, 0, None)
     assert rc == pcmm.PCMM_EDIM
     rc = L.pcmm_mul_cussen(None, 4, 4, 4, 4, 0, 4, None, None, None, 0, None)

@@ -360,3 +360,47 @@ def test_strassen_c64_every_output():
     exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, 64, 4)
     out = P.pcmm(cuda(I.A), cuda(ct), 64, 4, False, path=P.STRASSEN, iters=16).cpu().numpy()
     assert (out == exp).all()
+
+
+# ------------------------------------------------------------------ NEXT-1: wide plaintexts (t = 12, 16)
+@pytest.mark.parametrize("shape,t,signed", [((20, 24, 6), 12, False), ((33, 17, 5), 16, False),
+                                            ((16, 40, 3), 16, True), ((64, 64, 64), 16, False)])
+def test_wide_every_output(shape, t, signed):
+    # the paper's t = 12, 16 grid (Table A9): int32 plaintexts, up to min(m, 2^t - 1)
+    # distinct values per column; unsigned 16-bit values above 2^15 included
+    m, n, l = shape
+    cfg = synth.Config("wide", m, n, l, t, signed, 0, 255, 700 + m + t)
+    I = synth.make_instance(cfg)
+    A = I.A.copy()
+    if signed:
+        A[0, 0], A[1, 0], A[2, 0] = -(1 << (t - 1)), (1 << (t - 1)) - 1, 0
+    else:
+        A[0, 0], A[1, 0], A[2, 0] = (1 << t) - 1, 1 << (t - 1), 0
+    A[3, :] = A[4, :]                               # repeated rows / values
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.SCHOOLBOOK if m * n * l > 60000 else oracle.CUSSEN, A, ct, l, t)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        out = _gpu_pcmm(A, ct, l, t, signed, path)
+        assert (out == exp).all(), path
+
+
+def test_wide_chunked_equals_byte_path():
+    # the wide path at w <= 8 (several k-chunks forced by a tiny table budget) equals the
+    # byte path bit for bit, and an out-of-range plaintext is reported as EBOUND
+    import os
+    I = synth.make_instance(synth.CONFIGS["c64"], m=48, n=40, l=24, seed=77)
+    x = synth.keygen_secret(77)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    ref = _gpu_pcmm(I.A, ct, 24, 4, False, P.CUSSEN)
+    os.environ["PCMM_WIDE_BUDGET_MB"] = "1"
+    try:
+        out = _gpu_pcmm(I.A.astype(np.int32), ct, 24, 4, False, P.CUSSEN)
+    finally:
+        del os.environ["PCMM_WIDE_BUDGET_MB"]
+    assert (out == ref).all()
+    bad = I.A.astype(np.int32)
+    bad[5, 7] = 1 << 12
+    with pytest.raises(P.PCMMError) as e:
+        _gpu_pcmm(bad, ct, 24, 12, False, P.CUSSEN)
+    assert e.value.code == P.PCMM_EBOUND
