@@ -266,7 +266,8 @@ def main():
     m, n, l, w = cfg.m, cfg.n, cfg.l, cfg.w
     count = m * l
     path = {"cussen": P.CUSSEN, "schoolbook": P.SCHOOLBOOK, "strassen": P.STRASSEN}[args.path]
-    ws = P.alloc_workspace(m, n, l, w, path, dev)
+    wide = w > 8                         # int32 plaintexts: pcmm_mul_*_wide (NEXT-1, t = 12, 16)
+    ws = P.alloc_workspace(m, n, l, w, path, dev, wide=wide)
     proj = torch.empty(P.proj_bytes(count), dtype=torch.uint8, device=dev)
     out = torch.empty((count, 128), dtype=torch.uint8, device=dev)
     out_h = torch.empty((count, 128), dtype=torch.uint8).pin_memory()
@@ -373,14 +374,15 @@ def main():
         def sb():
             P.mul_schoolbook(A, ctB, l, w, cfg.signed, out_proj=proj, ws=ws_sb)
             P.normalize(proj, count, out=out)
-        ws_sb = P.alloc_workspace(m, n, l, w, P.SCHOOLBOOK, dev)
+        ws_sb = P.alloc_workspace(m, n, l, w, P.SCHOOLBOOK, dev, wide=wide)
+        ws_st = P.alloc_workspace(m, n, l, w, P.STRASSEN, dev, wide=wide)
         sb()
         ms_sb, _ = timed(sb, max(2, args.steps // 5))
         res["schoolbook"] = {"ms_per_step": ms_sb, "value": world * count / (ms_sb * 1e-3),
                              "cussen_speedup": ms_sb / ms}
 
         def st():
-            P.mul_strassen(A, ctB, l, w, cfg.signed, args.leaf, out_proj=proj, ws=ws_sb)
+            P.mul_strassen(A, ctB, l, w, cfg.signed, args.leaf, out_proj=proj, ws=ws_st)
             P.normalize(proj, count, out=out)
         st()
         ms_st, _ = timed(st, max(2, args.steps // 5))

@@ -134,7 +134,7 @@ PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int 
 
 /* Strassen PC-MM, the paper's second comparison path (Sec. 3.1,
  * PAPER.md:253-300): 7 half-size block PC-MMs per level (M1..M7), 5 plaintext
- * block sums / differences (int16 internally: entries grow one bit per level)
+ * block sums / differences (int32 internally: entries grow one bit per level)
  * and 13 ciphertext block additions / subtractions; recursion while m, n, l are
  * even and their halves >= `leaf`, then schoolbook on the blocks.  Output and
  * errors as pcmm_mul_schoolbook (workspace: path 2).  Temporary blocks are
@@ -155,7 +155,9 @@ PCMM_API int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, in
  * chunk's tables fit a 2 GiB budget (env PCMM_WIDE_BUDGET_MB overrides).
  * Output, status and errors as pcmm_mul_cussen / pcmm_mul_schoolbook, with
  * the workspace sized by pcmm_workspace_bytes_wide (path 0 schoolbook,
- * 1 Cussen; returns 0 for invalid arguments).  Async.                      */
+ * 1 Cussen, 2 Strassen; returns 0 for invalid arguments).  Async.
+ * pcmm_mul_strassen_wide: pcmm_mul_strassen for int32 plaintexts, w <= 16
+ * (the recursion's int32 block sums gain one bit per level).               */
 PCMM_API size_t pcmm_workspace_bytes_wide(int m, int n, int l, int w, int path);
 PCMM_API int pcmm_mul_cussen_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, int iters,
                                   const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes,
@@ -163,6 +165,9 @@ PCMM_API int pcmm_mul_cussen_wide(const int32_t *A_d, int m, int n, int l, int w
 PCMM_API int pcmm_mul_schoolbook_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed,
                                       const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes,
                                       void *stream);
+PCMM_API int pcmm_mul_strassen_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, int leaf,
+                                    const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes,
+                                    void *stream);
 
 /* Normalise `count` projective ciphertexts (layout above, as written by
  * pcmm_mul_*) to canonical affine bytes ctC_d[count][128] (x = X/Z, y = Y/Z,

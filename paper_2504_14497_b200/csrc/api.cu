@@ -314,26 +314,37 @@ int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, int is_si
                       (cudaStream_t)stream);
 }
 
-int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int leaf, const uint8_t *ctB_d,
-                      void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+static int mul_strassen(const void *A_d, int a_is_i32, int m, int n, int l, int w, int is_signed, int leaf,
+                        const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, cudaStream_t s) {
     g_err.clear();
     int rc = check_dims(m, n, l);
     if (rc) return rc;
     if (!A_d || !ctB_d || !ctC_proj_d || !ws_d) return fail(PCMM_EINVAL, "null pointer");
-    if (((uintptr_t)ctB_d & 15) || ((uintptr_t)ws_d & 255) || ((uintptr_t)ctC_proj_d & 15))
-        return fail(PCMM_EINVAL, "misaligned buffer (ctB/ctC 16 B, workspace 256 B)");
-    if (w < 1 || w > 8) return fail(PCMM_EINVAL, "w must be in [1, 8]");
+    if (((uintptr_t)ctB_d & 15) || ((uintptr_t)ws_d & 255) || ((uintptr_t)ctC_proj_d & 15) ||
+        (a_is_i32 && ((uintptr_t)A_d & 3)))
+        return fail(PCMM_EINVAL, "misaligned buffer (A 4 B if int32, ctB/ctC 16 B, workspace 256 B)");
+    if (w < 1 || w > (a_is_i32 ? 16 : 8)) return fail(PCMM_EINVAL, "w out of range (8 for int8 A, 16 for int32 A)");
     if (leaf < 1) return fail(PCMM_EINVAL, "leaf must be >= 1");
-    const Layout L = layout(m, n, l, w, PCMM_PATH_STRASSEN);
+    const Layout L = layout(m, n, l, 1, PCMM_PATH_STRASSEN);
     if (ws_bytes < L.total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_workspace_bytes)");
-    cudaStream_t s = (cudaStream_t)stream;
     uint8_t *ws = (uint8_t *)ws_d;
     int *status = (int *)ws;
     uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
     CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
     LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
-    LAUNCH("strassen", s, run_strassen(A_d, m, n, l, w, is_signed, bsoa, leaf, (uint32_t *)ctC_proj_d, status, s));
+    LAUNCH("strassen", s,
+           run_strassen(A_d, a_is_i32, m, n, l, w, is_signed, bsoa, leaf, (uint32_t *)ctC_proj_d, status, s));
     return PCMM_OK;
+}
+
+int pcmm_mul_strassen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int leaf, const uint8_t *ctB_d,
+                      void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_strassen(A_d, 0, m, n, l, w, is_signed, leaf, ctB_d, ctC_proj_d, ws_d, ws_bytes, (cudaStream_t)stream);
+}
+
+int pcmm_mul_strassen_wide(const int32_t *A_d, int m, int n, int l, int w, int is_signed, int leaf,
+                           const uint8_t *ctB_d, void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream) {
+    return mul_strassen(A_d, 1, m, n, l, w, is_signed, leaf, ctB_d, ctC_proj_d, ws_d, ws_bytes, (cudaStream_t)stream);
 }
 
 int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
@@ -343,7 +354,9 @@ int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed
 }
 
 size_t pcmm_workspace_bytes_wide(int m, int n, int l, int w, int path) {
-    if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 16 || m > kWideMaxM) return 0;
+    if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 16) return 0;
+    if (path == PCMM_PATH_STRASSEN) return layout(m, n, l, 1, PCMM_PATH_STRASSEN).total;
+    if (m > kWideMaxM) return 0;
     if (path != PCMM_PATH_SCHOOLBOOK && path != PCMM_PATH_CUSSEN) return 0;
     return layout_wide(m, n, l, w, path).total;
 }

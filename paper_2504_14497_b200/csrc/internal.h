@@ -70,8 +70,8 @@ cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const 
                               int64_t count, cudaStream_t s);
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s);
 int num_sms();
-cudaError_t run_strassen(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa, int leaf,
-                         uint32_t *out, int *status, cudaStream_t s);
+cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w, int is_signed,
+                         const uint32_t *bsoa, int leaf, uint32_t *out, int *status, cudaStream_t s);
 int accum_ctas_per_sm(int slots);
 // wide-plaintext path (wide.cu, hot.cu k_accum_gw): t <= 16, int32 A, uint16 rank, k-chunked tables
 int wide_plan_p2(int m);

@@ -2,7 +2,7 @@
 // arXiv 2504.14497 Sec. 3.1).
 //
 // Breadth-first schedule: level d holds all 7^d subproblems and each step of a
-// level is one batched launch (k_down_a, k_down_b, k_school16_batched, k_up_c).
+// level is one batched launch (k_down_a, k_down_b, k_school_batched, k_up_c).
 // One recursion level splits A (plaintext), Enc(B) and Enc(C) into 2 x 2 blocks
 // and forms
 //   M1 = (A11 + A22)(B11 + B22)   M2 = (A21 + A22) B11     M3 = A11 (B12 - B22)
@@ -13,7 +13,7 @@
 // ciphertext block additions / subtractions.  The recursion stops
 // at blocks of <= `leaf` rows / inner / columns (or an odd dimension) and runs the
 // schoolbook kernel there.  Plaintext sums grow by one bit per level, so the
-// recursion carries int16 plaintexts; ciphertext blocks are projective
+// recursion carries int32 plaintexts; ciphertext blocks are projective
 // Montgomery SoA ([c][X,Y,Z][limb][r * cols + col]).
 #include <vector>
 
@@ -42,17 +42,24 @@ __device__ __forceinline__ void soa_st(uint32_t *base, int64_t stride, int64_t i
     }
 }
 
-// widen A to int16 and check the w-bit range (EBOUND)
-__global__ void k_a_widen(const int8_t *__restrict__ A, int64_t count, int w, int is_signed,
-                          int16_t *__restrict__ out, int *__restrict__ status) {
+// widen A to int32 and check the w-bit range (EBOUND); A is int8 / uint8 (byte
+// API) or int32 (wide API, w <= 16)
+__device__ __forceinline__ int a_value(const int8_t *A, int64_t t, int is_signed) {
+    return is_signed ? (int)A[t] : (int)(uint8_t)A[t];
+}
+__device__ __forceinline__ int a_value(const int32_t *A, int64_t t, int) { return A[t]; }
+
+template <typename TA>
+__global__ void k_a_widen(const TA *__restrict__ A, int64_t count, int w, int is_signed,
+                          int32_t *__restrict__ out, int *__restrict__ status) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= count) return;
-    const int v = is_signed ? (int)A[t] : (int)(uint8_t)A[t];
+    const int v = a_value(A, t, is_signed);
     const int lo = is_signed ? -(1 << (w - 1)) : 0;
     const int hi = is_signed ? (1 << (w - 1)) - 1 : (1 << w) - 1;
     const bool ok = v >= lo && v <= hi;
     if (!ok) atomicOr(status, kStatusBound);
-    out[t] = (int16_t)(ok ? v : 0);
+    out[t] = ok ? v : 0;
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -67,7 +74,7 @@ __constant__ int8_t kCoefC[4][7] = {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0
                                     {0, 1, 0, 1, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0}};
 
 // level d -> d+1 plaintext operands: child (p*7+q) = sum_b coefA[q][b] * block_b(parent p)
-__global__ void k_down_a(const int16_t *__restrict__ A, int64_t P, int h, int w, int16_t *__restrict__ out) {
+__global__ void k_down_a(const int32_t *__restrict__ A, int64_t P, int h, int w, int32_t *__restrict__ out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t per = (int64_t)h * w;
     if (t >= P * 7 * per) return;
@@ -75,14 +82,14 @@ __global__ void k_down_a(const int16_t *__restrict__ A, int64_t P, int h, int w,
     const int64_t p = child / 7;
     const int q = (int)(child % 7);
     const int r = (int)(e / w), c = (int)(e % w);
-    const int16_t *Ap = A + p * 4 * per;              // parent is (2h) x (2w), row-major
+    const int32_t *Ap = A + p * 4 * per;              // parent is (2h) x (2w), row-major
     int v = 0;
 #pragma unroll
     for (int b = 0; b < 4; b++) {
         const int co = kCoefA[q][b];
         if (co) v += co * (int)Ap[(int64_t)((b >> 1) * h + r) * (2 * w) + (b & 1) * w + c];
     }
-    out[t] = (int16_t)v;
+    out[t] = (int32_t)v;
 }
 
 // level d -> d+1 ciphertext operands (at most two blocks per combination: one point op)
@@ -149,8 +156,8 @@ __global__ void k_up_c(const uint32_t *__restrict__ M, int64_t P, int h, int w, 
 }
 
 // batched leaf schoolbook: problem z / 2, component z % 2; problem p's A block is
-// A + p m n (int16), its B block starts at index p n l of the level's SoA
-__global__ void __launch_bounds__(128) k_school16_batched(const int16_t *__restrict__ A, int m, int n, int l,
+// A + p m n (int32), its B block starts at index p n l of the level's SoA
+__global__ void __launch_bounds__(128) k_school_batched(const int32_t *__restrict__ A, int m, int n, int l,
                                                          int64_t P, const uint32_t *__restrict__ B,
                                                          uint32_t *__restrict__ out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(128) k_school16_batched(const int16_t *__restr
     const int jj = min(j, l - 1);
     const int64_t cnt = P * n * l;
     const uint32_t *bc = B + (int64_t)c * kPtWords * cnt + p * n * l;
-    const int16_t *Ap = A + p * m * n;
+    const int32_t *Ap = A + p * m * n;
     pt acc, X, T;
     pt_identity(acc);
     for (int k = 0; k < n; k++) {
@@ -184,8 +191,8 @@ __global__ void __launch_bounds__(128) k_school16_batched(const int16_t *__restr
 
 }  // namespace
 
-cudaError_t run_strassen(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa, int leaf,
-                         uint32_t *out, int *status, cudaStream_t s) {
+cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w, int is_signed,
+                         const uint32_t *bsoa, int leaf, uint32_t *out, int *status, cudaStream_t s) {
     // breadth-first: level d holds all 7^d subproblems, so every step of a level is
     // ONE batched launch (a GPU-friendly schedule of the same Strassen recursion)
     if (leaf < 1) leaf = 1;
@@ -197,17 +204,22 @@ cudaError_t run_strassen(const int8_t *A, int m, int n, int l, int w, int is_sig
     auto note = [&](cudaError_t e) {
         if (err == cudaSuccess && e != cudaSuccess) err = e;
     };
-    std::vector<int16_t *> As(D + 1, nullptr);
+    std::vector<int32_t *> As(D + 1, nullptr);
     std::vector<uint32_t *> Bs(D + 1, nullptr), Cs(D + 1, nullptr);
     int64_t P = 1;
-    note(cudaMallocAsync((void **)&As[0], (size_t)m * n * 2 + 2, s));
+    note(cudaMallocAsync((void **)&As[0], (size_t)m * n * 4 + 4, s));
     if (err) return err;
-    k_a_widen<<<nblk((int64_t)m * n, 256), 256, 0, s>>>(A, (int64_t)m * n, w, is_signed, As[0], status);
+    if (a_is_i32)
+        k_a_widen<int32_t><<<nblk((int64_t)m * n, 256), 256, 0, s>>>((const int32_t *)A, (int64_t)m * n, w,
+                                                                     is_signed, As[0], status);
+    else
+        k_a_widen<int8_t><<<nblk((int64_t)m * n, 256), 256, 0, s>>>((const int8_t *)A, (int64_t)m * n, w,
+                                                                    is_signed, As[0], status);
     note(cudaGetLastError());
     Bs[0] = const_cast<uint32_t *>(bsoa);
     for (int d = 0; d < D && err == cudaSuccess; d++) {               // down: operands of the 7 products
         const int h = m >> (d + 1), kk = n >> (d + 1), ww = l >> (d + 1);
-        note(cudaMallocAsync((void **)&As[d + 1], (size_t)P * 7 * h * kk * 2 + 2, s));
+        note(cudaMallocAsync((void **)&As[d + 1], (size_t)P * 7 * h * kk * 4 + 4, s));
         note(cudaMallocAsync((void **)&Bs[d + 1], (size_t)P * 7 * kk * ww * 2 * kPtWords * 4, s));
         if (err) break;
         k_down_a<<<nblk(P * 7 * h * kk, 256), 256, 0, s>>>(As[d], P, h, kk, As[d + 1]);
@@ -222,7 +234,7 @@ cudaError_t run_strassen(const int8_t *A, int m, int n, int l, int w, int is_sig
         else note(cudaMallocAsync((void **)&Cs[D], (size_t)P * mD * lD * 2 * kPtWords * 4, s));
         if (err == cudaSuccess) {
             dim3 grid((unsigned)((int64_t)nblk(lD, 32) * nblk(mD, 4) * 2 * P));
-            k_school16_batched<<<grid, 128, 0, s>>>(As[D], mD, nD, lD, P, Bs[D], Cs[D]);
+            k_school_batched<<<grid, 128, 0, s>>>(As[D], mD, nD, lD, P, Bs[D], Cs[D]);
             note(cudaGetLastError());
         }
     }

@@ -33,6 +33,7 @@ EXPORTS = [
     "pcmm_mul_schoolbook", "pcmm_mul_cussen", "pcmm_mul_strassen", "pcmm_normalize", "pcmm_decrypt_small", "pcmm_status",
     "pcmm_profile_enable", "pcmm_profile_read", "pcmm_test_field", "pcmm_test_point", "pcmm_test_plan",
     "pcmm_bench_fp_mul", "pcmm_workspace_bytes_wide", "pcmm_mul_cussen_wide", "pcmm_mul_schoolbook_wide",
+    "pcmm_mul_strassen_wide",
 ]
 
 
@@ -85,6 +86,7 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
             L.pcmm_workspace_bytes_wide.argtypes = [i32] * 5
             L.pcmm_mul_cussen_wide.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             L.pcmm_mul_schoolbook_wide.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+            L.pcmm_mul_strassen_wide.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             _lib = L
     return _lib
 
@@ -185,8 +187,6 @@ def _mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signe
     if out_proj is None:
         out_proj = torch.empty(proj_bytes(m * l), dtype=torch.uint8, device=A.device)
     if A.dtype == torch.int32:                     # wide plaintexts (w <= 16): pcmm_mul_*_wide
-        if path == STRASSEN:
-            raise PCMMError(PCMM_ENOTSUP, "Strassen takes int8 / uint8 plaintexts only")
         if ws is None:
             ws = alloc_workspace(m, n, l, w, path, A.device, wide=True)
         L = load()
@@ -194,6 +194,9 @@ def _mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, is_signe
         if path == SCHOOLBOOK:
             rc = L.pcmm_mul_schoolbook_wide(*a, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(), ws.data_ptr(),
                                             ws.numel(), _stream(stream))
+        elif path == STRASSEN:
+            rc = L.pcmm_mul_strassen_wide(*a, iters, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(),
+                                          ws.data_ptr(), ws.numel(), _stream(stream))
         else:
             rc = L.pcmm_mul_cussen_wide(*a, iters, _dev(ctB, torch.uint8, "ctB"), out_proj.data_ptr(),
                                         ws.data_ptr(), ws.numel(), _stream(stream))

@@ -383,6 +383,8 @@ def test_wide_every_output(shape, t, signed):
     for path in (P.CUSSEN, P.SCHOOLBOOK):
         out = _gpu_pcmm(A, ct, l, t, signed, path)
         assert (out == exp).all(), path
+    if m % 2 == 0 and n % 2 == 0 and l % 2 == 0:
+        assert (_gpu_pcmm(A, ct, l, t, signed, P.STRASSEN, iters=4) == exp).all()   # leaf 4
 
 
 def test_wide_chunked_equals_byte_path():
