@@ -176,6 +176,42 @@ PCMM_API int pcmm_mul_strassen_wide(const int32_t *A_d, int m, int n, int l, int
 PCMM_API int pcmm_normalize(const void *ctC_proj_d, int64_t count, uint8_t *ctC_d, void *ws_d, size_t ws_bytes,
                    void *stream);
 
+/* ---- NEXT-2: fixed-base comb encryption ---------------
+ * Encrypt with per-key precomputed tables: a context holds
+ * T_P[i][v] = v 2^(8i) P for P in {G, H = pk}, 32 byte windows i, v < 256,
+ * affine Montgomery (1 MiB + 256 B, pcmm_enc_ctx_bytes()); then
+ *   C1 = r G = sum_i T_G[i][r_i],  C2 = r H + b G = sum_i T_H[i][r_i] +- sum_{i<4} T_G[i][|b|_i]
+ * (Jacobian + affine mixed additions with a complete fallback, one inversion
+ * per ciphertext).  Output bytes are identical to pcmm_encrypt.
+ *   pcmm_enc_ctx_init: ctx_d caller-owned device memory (256-byte aligned,
+ *     pcmm_enc_ctx_bytes() bytes); builds the tables on `stream` and
+ *     SYNCHRONISES it.  ENOTONCURVE if pk is not a P-256 point (or is 0).
+ *   pcmm_encrypt_ctx: as pcmm_encrypt (b_d int32, r_d count x 32 B BE in
+ *     [1, q-1], ct_d count x 128 B; r_d / ct_d 16-byte aligned).  Async.   */
+PCMM_API size_t pcmm_enc_ctx_bytes(void);
+PCMM_API int pcmm_enc_ctx_init(const uint8_t pk_h[64], void *ctx_d, void *stream);
+PCMM_API int pcmm_encrypt_ctx(const void *ctx_d, const int32_t *b_d, const uint8_t *r_d, int64_t count,
+                              uint8_t *ct_d, void *stream);
+
+/* ---- NEXT-2: baby-step giant-step decryption ----------------------------
+ * Decrypt for messages in [lo, hi] with a device hash
+ * table of the baby steps { j G : 1 <= j < s = 2^log2_baby } (open addressing,
+ * 2s slots, key = affine x with the parity of y, so jG and -jG differ):
+ *   pcmm_bsgs_ctx_bytes(log2_baby) = 256 + 24 s bytes (0 if log2_baby is
+ *     outside [1, 28]);
+ *   pcmm_bsgs_init: builds the table into ctx_d (256-byte aligned). Async.
+ *   pcmm_decrypt_bsgs: per ciphertext M = C2 - x C1 - lo G, giant steps
+ *     M - i s G (batches of 8 sharing one inversion) until the identity (j = 0)
+ *     or a table hit j: m = lo + i s + j.  (hi - lo + 1) / s <= 2^24 and
+ *     |lo|, |hi| < 2^62.  m_d / status_d as pcmm_decrypt_small (status 0,
+ *     PCMM_EDECODE if m is not in [lo, hi], PCMM_ENOTONCURVE for a bad input).
+ *     Async.  Errors: EINVAL, ECUDA.                                         */
+PCMM_API size_t pcmm_bsgs_ctx_bytes(int log2_baby);
+PCMM_API int pcmm_bsgs_init(int log2_baby, void *ctx_d, void *stream);
+PCMM_API int pcmm_decrypt_bsgs(const uint8_t sk_h[32], const void *ctx_d, int log2_baby, const uint8_t *ct_d,
+                               int64_t count, int64_t lo, int64_t hi, int64_t *m_d, int32_t *status_d,
+                               void *stream);
+
 /* Decrypt: m_e = phi^-1(C2 - x C1) by an exact lookup in
  * the table { m G : lo <= m <= hi } (hi - lo < 2^26).  sk_h = x (32 B BE).
  * m_d[e] receives the message, status_d[e] = 0 or PCMM_EDECODE if no m in

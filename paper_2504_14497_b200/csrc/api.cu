@@ -464,6 +464,73 @@ int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t coun
     return rc;
 }
 
+// ---------------------------------------------------------------- NEXT-2
+size_t pcmm_enc_ctx_bytes(void) { return enc_ctx_bytes(); }
+
+int pcmm_enc_ctx_init(const uint8_t pk_h[64], void *ctx_d, void *stream) {
+    g_err.clear();
+    if (!pk_h || !ctx_d) return fail(PCMM_EINVAL, "null pointer");
+    if ((uintptr_t)ctx_d & 255) return fail(PCMM_EINVAL, "context must be 256-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("enc_ctx_init", s, launch_enc_ctx_init(pk_h, (uint32_t *)ctx_d, s));
+    uint32_t hdr[2] = {0, 0};
+    CK(cudaMemcpyAsync(hdr, ctx_d, 8, cudaMemcpyDeviceToHost, s), "header copy");
+    CK(cudaStreamSynchronize(s), "stream sync");
+    if (hdr[1] != 1) {
+        CK(cudaMemsetAsync(ctx_d, 0, 4, s), "clear magic");
+        return fail(PCMM_ENOTONCURVE, "public key is not a point of P-256 (or is the identity)");
+    }
+    return PCMM_OK;
+}
+
+int pcmm_encrypt_ctx(const void *ctx_d, const int32_t *b_d, const uint8_t *r_d, int64_t count, uint8_t *ct_d,
+                     void *stream) {
+    g_err.clear();
+    if (count < 0) return fail(PCMM_EINVAL, "count < 0");
+    if (count == 0) return PCMM_OK;
+    if (!ctx_d || !b_d || !r_d || !ct_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)r_d & 15) || ((uintptr_t)ct_d & 15) || ((uintptr_t)ctx_d & 255))
+        return fail(PCMM_EINVAL, "misaligned buffer (r / ct 16 B, context 256 B)");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("encrypt_comb", s, launch_encrypt_comb((const uint32_t *)ctx_d, b_d, r_d, count, ct_d, s));
+    return PCMM_OK;
+}
+
+size_t pcmm_bsgs_ctx_bytes(int log2_baby) {
+    if (log2_baby < 1 || log2_baby > 28) return 0;
+    return bsgs_ctx_bytes(log2_baby);
+}
+
+int pcmm_bsgs_init(int log2_baby, void *ctx_d, void *stream) {
+    g_err.clear();
+    if (log2_baby < 1 || log2_baby > 28) return fail(PCMM_EINVAL, "log2_baby must be in [1, 28]");
+    if (!ctx_d) return fail(PCMM_EINVAL, "null pointer");
+    if ((uintptr_t)ctx_d & 255) return fail(PCMM_EINVAL, "context must be 256-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    LAUNCH("bsgs_init", s, launch_bsgs_init(log2_baby, (uint32_t *)ctx_d, s));
+    return PCMM_OK;
+}
+
+int pcmm_decrypt_bsgs(const uint8_t sk_h[32], const void *ctx_d, int log2_baby, const uint8_t *ct_d, int64_t count,
+                      int64_t lo, int64_t hi, int64_t *m_d, int32_t *status_d, void *stream) {
+    g_err.clear();
+    if (count < 0 || hi < lo) return fail(PCMM_EINVAL, "count < 0 or hi < lo");
+    if (log2_baby < 1 || log2_baby > 28) return fail(PCMM_EINVAL, "log2_baby must be in [1, 28]");
+    if (lo <= -(1LL << 62) || hi >= (1LL << 62)) return fail(PCMM_EINVAL, "|lo|, |hi| must be < 2^62");
+    const uint64_t range = (uint64_t)(hi - lo) + 1;
+    if ((range >> log2_baby) > (1ULL << 24)) return fail(PCMM_EINVAL, "range > 2^24 giant steps of 2^log2_baby");
+    if (count == 0) return PCMM_OK;
+    if (!sk_h || !ctx_d || !ct_d || !m_d || !status_d) return fail(PCMM_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t x[8];
+    for (int i = 0; i < 8; i++) {
+        const uint8_t *p = sk_h + 28 - 4 * i;
+        x[i] = ((uint32_t)p[0] << 24) | ((uint32_t)p[1] << 16) | ((uint32_t)p[2] << 8) | p[3];
+    }
+    LAUNCH("decrypt_bsgs", s, launch_decrypt_bsgs(x, (const uint32_t *)ctx_d, ct_d, count, lo, hi, m_d, status_d, s));
+    return PCMM_OK;
+}
+
 int pcmm_status(const void *ws_d, void *stream) {
     g_err.clear();
     if (!ws_d) return fail(PCMM_EINVAL, "null workspace");

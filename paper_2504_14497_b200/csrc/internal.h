@@ -73,6 +73,15 @@ int num_sms();
 cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w, int is_signed,
                          const uint32_t *bsoa, int leaf, uint32_t *out, int *status, cudaStream_t s);
 int accum_ctas_per_sm(int slots);
+// NEXT-2 (next2.cu): fixed-base comb encryption context, BSGS decryption context
+size_t enc_ctx_bytes();
+cudaError_t launch_enc_ctx_init(const uint8_t pk[64], uint32_t *ctx, cudaStream_t s);   // synchronises s
+cudaError_t launch_encrypt_comb(const uint32_t *ctx, const int32_t *b, const uint8_t *r, int64_t count, uint8_t *ct,
+                                cudaStream_t s);
+size_t bsgs_ctx_bytes(int log2s);
+cudaError_t launch_bsgs_init(int log2s, uint32_t *ctx, cudaStream_t s);
+cudaError_t launch_decrypt_bsgs(const uint32_t x[8], const uint32_t *ctx, const uint8_t *ct, int64_t count,
+                                int64_t lo, int64_t hi, int64_t *m, int32_t *status, cudaStream_t s);
 // wide-plaintext path (wide.cu, hot.cu k_accum_gw): t <= 16, int32 A, uint16 rank, k-chunked tables
 int wide_plan_p2(int m);
 size_t wide_plan_smem(int m, int cap);

@@ -33,7 +33,8 @@ EXPORTS = [
     "pcmm_mul_schoolbook", "pcmm_mul_cussen", "pcmm_mul_strassen", "pcmm_normalize", "pcmm_decrypt_small", "pcmm_status",
     "pcmm_profile_enable", "pcmm_profile_read", "pcmm_test_field", "pcmm_test_point", "pcmm_test_plan",
     "pcmm_bench_fp_mul", "pcmm_workspace_bytes_wide", "pcmm_mul_cussen_wide", "pcmm_mul_schoolbook_wide",
-    "pcmm_mul_strassen_wide",
+    "pcmm_mul_strassen_wide", "pcmm_enc_ctx_bytes", "pcmm_enc_ctx_init", "pcmm_encrypt_ctx", "pcmm_bsgs_ctx_bytes",
+    "pcmm_bsgs_init", "pcmm_decrypt_bsgs",
 ]
 
 
@@ -87,6 +88,14 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
             L.pcmm_mul_cussen_wide.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             L.pcmm_mul_schoolbook_wide.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
             L.pcmm_mul_strassen_wide.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+            L.pcmm_enc_ctx_bytes.restype = sz
+            L.pcmm_enc_ctx_bytes.argtypes = []
+            L.pcmm_enc_ctx_init.argtypes = [vp, vp, vp]
+            L.pcmm_encrypt_ctx.argtypes = [vp, vp, vp, i64, vp, vp]
+            L.pcmm_bsgs_ctx_bytes.restype = sz
+            L.pcmm_bsgs_ctx_bytes.argtypes = [i32]
+            L.pcmm_bsgs_init.argtypes = [i32, vp, vp]
+            L.pcmm_decrypt_bsgs.argtypes = [vp, vp, i32, vp, i64, i64, i64, vp, vp, vp]
             _lib = L
     return _lib
 
@@ -154,6 +163,52 @@ def decrypt_small(sk: bytes, ct: torch.Tensor, lo: int, hi: int, stream=None):
     skb = ctypes.create_string_buffer(bytes(sk), 32)
     _check(load().pcmm_decrypt_small(skb, _dev(ct, torch.uint8, "ct"), count, lo, hi, m.data_ptr(), st.data_ptr(),
                                      _stream(stream)))
+    return m, st
+
+
+# ------------------------------------------------------------------ NEXT-2: comb encryption, BSGS decryption
+def enc_ctx(pk: bytes, device="cuda", stream=None) -> torch.Tensor:
+    """Fixed-base comb tables for G and H = pk: a device context (synchronises the stream)."""
+    _require_cuda()
+    ctx = torch.empty(int(load().pcmm_enc_ctx_bytes()), dtype=torch.uint8, device=device)
+    pkb = ctypes.create_string_buffer(bytes(pk), 64)
+    _check(load().pcmm_enc_ctx_init(pkb, ctx.data_ptr(), _stream(stream)))
+    return ctx
+
+
+def encrypt_ctx(ctx: torch.Tensor, b: torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """Encrypt with a comb context: same bytes as `encrypt` (b int32 [count], r uint8 [count, 32])."""
+    _require_cuda()
+    count = b.numel()
+    if r.numel() != 32 * count:
+        raise PCMMError(PCMM_EINVAL, "r must hold 32 bytes per plaintext")
+    if out is None:
+        out = torch.empty((count, 128), dtype=torch.uint8, device=b.device)
+    _check(load().pcmm_encrypt_ctx(_dev(ctx, torch.uint8, "ctx"), _dev(b, torch.int32, "b"),
+                                   _dev(r, torch.uint8, "r"), count, _dev(out, torch.uint8, "out"), _stream(stream)))
+    return out
+
+
+def bsgs_ctx(log2_baby: int, device="cuda", stream=None) -> torch.Tensor:
+    """Baby-step table { jG : 1 <= j < 2^log2_baby } as a device hash table."""
+    _require_cuda()
+    nb = int(load().pcmm_bsgs_ctx_bytes(log2_baby))
+    if nb == 0:
+        raise PCMMError(PCMM_EINVAL, "log2_baby must be in [1, 28]")
+    ctx = torch.empty(nb, dtype=torch.uint8, device=device)
+    _check(load().pcmm_bsgs_init(log2_baby, ctx.data_ptr(), _stream(stream)))
+    return ctx
+
+
+def decrypt_bsgs(sk: bytes, ctx: torch.Tensor, log2_baby: int, ct: torch.Tensor, lo: int, hi: int, stream=None):
+    """Decrypt messages in [lo, hi] by baby-step giant-step -> (m int64, status int32)."""
+    _require_cuda()
+    count = ct.numel() // 128
+    m = torch.empty(count, dtype=torch.int64, device=ct.device)
+    st = torch.empty(count, dtype=torch.int32, device=ct.device)
+    skb = ctypes.create_string_buffer(bytes(sk), 32)
+    _check(load().pcmm_decrypt_bsgs(skb, _dev(ctx, torch.uint8, "ctx"), log2_baby, _dev(ct, torch.uint8, "ct"),
+                                    count, lo, hi, m.data_ptr(), st.data_ptr(), _stream(stream)))
     return m, st
 
 

@@ -406,3 +406,73 @@ def test_wide_chunked_equals_byte_path():
     with pytest.raises(P.PCMMError) as e:
         _gpu_pcmm(bad, ct, 24, 12, False, P.CUSSEN)
     assert e.value.code == P.PCMM_EBOUND
+
+
+# ------------------------------------------------------------------ NEXT-2: comb encryption, BSGS decryption
+def test_encrypt_comb_matches_oracle():
+    x = synth.keygen_secret(31)
+    pk = ecref.mulG(x)
+    ctx = P.enc_ctx(pk)
+    g = synth.SplitMix64(31)
+    count = 3000
+    b = g.small(-(2**31), 2**31 - 1, count)
+    b[:8] = [0, 1, -1, 2**31 - 1, -(2**31), 255, -256, 65536]
+    b = b.astype(np.int32)
+    rs = g.scalars256(count)
+    rs[:6] = [1, ecref.Q - 1, 2**255, 256, 2**64 - 1, 0x0100000000000000000000000000000000000000000000000000000000000001]
+    r_be = synth.scalars_to_be_bytes(rs)
+    exp = oracle.encrypt(pk, b, r_be)
+    out = P.encrypt_ctx(ctx, cuda(b), cuda(r_be)).cpu().numpy()
+    assert (out == exp).all()
+    assert (P.encrypt(pk, cuda(b), cuda(r_be)).cpu().numpy() == exp).all()
+
+
+def test_enc_ctx_rejects_bad_key():
+    bad = bytearray(ecref.mulG(5))
+    bad[63] ^= 1
+    with pytest.raises(P.PCMMError) as e:
+        P.enc_ctx(bytes(bad))
+    assert e.value.code == P.PCMM_ENOTONCURVE
+    with pytest.raises(P.PCMMError) as e:
+        P.enc_ctx(bytes(64))
+    assert e.value.code == P.PCMM_ENOTONCURVE
+
+
+def test_decrypt_bsgs_ranges():
+    x = synth.keygen_secret(32)
+    sk = x.to_bytes(32, "big")
+    pk = ecref.mulG(x)
+    g = synth.SplitMix64(32)
+    lo, hi = -(2**29) + 7, 2**30 - 3
+    s = 2**20
+    msgs = [lo, hi, lo + s, lo + 5 * s, lo + 5 * s - 1, 0, 1, -1, lo + 1, hi - 1]
+    msgs += [int(v) for v in g.small(lo, hi, 200)]
+    out_of_range = [lo - 1, hi + 1, -(2**31), 2**31 - 1]
+    b = np.array(msgs + out_of_range, dtype=np.int64).astype(np.int32)
+    ct = oracle.encrypt(pk, b, synth.scalars_to_be_bytes(g.scalars256(len(b))))
+    ctx = P.bsgs_ctx(20)
+    m, st = P.decrypt_bsgs(sk, ctx, 20, cuda(ct), lo, hi)
+    m, st = m.cpu().numpy(), st.cpu().numpy()
+    n_in = len(msgs)
+    assert (st[:n_in] == 0).all() and (m[:n_in] == np.array(msgs)).all()
+    assert (st[n_in:] == P.PCMM_EDECODE).all()
+    # agrees with the exact-table decryption on a small range, and reports a bad point
+    small = np.array([-5, 0, 3, 100, 999], dtype=np.int32)
+    ct2 = oracle.encrypt(pk, small, synth.scalars_to_be_bytes(g.scalars256(5)))
+    ct2[4, 100] ^= 1
+    m1, s1 = P.decrypt_small(sk, cuda(ct2), -10, 1000)
+    m2, s2 = P.decrypt_bsgs(sk, ctx, 20, cuda(ct2), -10, 1000)
+    assert (m1.cpu() == m2.cpu()).all() and (s1.cpu() == s2.cpu()).all()
+    assert list(s2.cpu().numpy()) == [0, 0, 0, 0, P.PCMM_ENOTONCURVE]
+
+
+def test_pcmm_output_decrypts_with_bsgs():
+    I = synth.make_instance(synth.CONFIGS["c64"], m=16, n=64, l=8, seed=33)
+    sk, pk = P.keygen(33)
+    ctx = P.enc_ctx(pk)
+    ct = P.encrypt_ctx(ctx, cuda(I.B.reshape(-1).astype(np.int32)), cuda(I.r_be))
+    out = P.pcmm(cuda(I.A), ct, 8, 4, False, P.CUSSEN)
+    bctx = P.bsgs_ctx(12)
+    m, st = P.decrypt_bsgs(sk, bctx, 12, out, 0, 64 * 15 * 255)
+    assert (st.cpu().numpy() == 0).all()
+    assert (m.cpu().numpy().reshape(16, 8) == I.A.astype(np.int64) @ I.B.astype(np.int64)).all()
