@@ -162,3 +162,68 @@ def make_instance(cfg: Config, m: int | None = None, n: int | None = None, l: in
 def keygen_secret(seed: int) -> int:
     """The secret key x that `make_instance(seed=...)` (and pcmm_keygen) derive."""
     return SplitMix64(seed).scalar256()
+
+
+# ------------------------------------------------------------- NEXT-4: Paillier key material
+def _probable_prime(v: int, g: "SplitMix64", rounds: int = 24) -> bool:
+    """Miller-Rabin with bases drawn from `g` (key material only, not the method's arithmetic)."""
+    if v < 4:
+        return v in (2, 3)
+    if v % 2 == 0:
+        return False
+    for sp in (3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if v % sp == 0:
+            return v == sp
+    d, s = v - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for _ in range(rounds):
+        a = 2 + g.next() % (v - 3)
+        x = pow(a, d, v)
+        if x in (1, v - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % v
+            if x == v - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def paillier_primes(seed: int, nbits: int) -> tuple[int, int]:
+    """Deterministic primes p != q of nbits/2 bits each (top two bits set so that n = p q has
+    exactly nbits bits) with gcd(p q, (p-1)(q-1)) = 1."""
+    from math import gcd
+    g = SplitMix64(seed ^ 0x5A5A5A5A5A5A5A5A)
+    half = nbits // 2
+    out = []
+    while len(out) < 2:
+        words = [g.next() for _ in range((half + 63) // 64)]
+        v = 0
+        for w in words:
+            v = (v << 64) | w
+        v &= (1 << half) - 1
+        v |= (3 << (half - 2)) | 1
+        if _probable_prime(v, g) and v not in out:
+            out.append(v)
+    p, q = out
+    assert gcd(p * q, (p - 1) * (q - 1)) == 1
+    return p, q
+
+
+def paillier_random_units(seed: int, n: int, count: int) -> list[int]:
+    """`count` values r in [1, n-1] with gcd(r, n) = 1 (encryption randomness)."""
+    from math import gcd
+    g = SplitMix64(seed ^ 0x3C3C3C3C3C3C3C3C)
+    words = (n.bit_length() + 63) // 64
+    out = []
+    while len(out) < count:
+        v = 0
+        for _ in range(words):
+            v = (v << 64) | g.next()
+        v %= n
+        if v and gcd(v, n) == 1:
+            out.append(v)
+    return out
