@@ -176,6 +176,28 @@ PCMM_API int pcmm_mul_strassen_wide(const int32_t *A_d, int m, int n, int l, int
 PCMM_API int pcmm_normalize(const void *ctC_proj_d, int64_t count, uint8_t *ctC_d, void *ws_d, size_t ws_bytes,
                    void *stream);
 
+/* ---- NEXT-4: PC-MM over the Paillier scheme -----------
+ * Sec. 2.5 and the extension of PAPER.md:585-626: with
+ * Eq. 6 the product is C_ij = prod_k c_kj^{a_ik} mod n^2;
+ * path 0 = schoolbook (one Alg. 4 Montgomery powering ladder of w steps per
+ * term), path 1 = Cussen (Alg. 3 with point additions ->
+ * modular multiplications and ECSMs -> Alg. 4 exponentiations, `iters` = N).
+ *   A_d   : uint8[m][n], non-negative plaintexts < 2^w, w in [1, 8]
+ *           (negative scalars would need c^-1 mod n^2; R20);
+ *   N2_h  : HOST pointer to the modulus n^2, nbits_n2 / 32 little-endian
+ *           32-bit words, odd; nbits_n2 in {512, 1024, 2048, 3072};
+ *   ctB_d : uint32[n*l][nbits_n2/32] ciphertexts (residues < n^2, words
+ *           little-endian, (k, j) row-major);
+ *   ctC_d : uint32[m*l][nbits_n2/32] output residues, (i, j) row-major.
+ * Workspace: pcmm_paillier_workspace_bytes (0 for invalid arguments).
+ * Async.  Device-side status via pcmm_status(ws_d): EBOUND (a_ik >= 2^w),
+ * ENOTONCURVE (a ciphertext >= n^2).  Errors: EINVAL, EDIM, ENOMEM,
+ * ENOTSUP (modulus size / iters), ECUDA.                                    */
+PCMM_API size_t pcmm_paillier_workspace_bytes(int m, int n, int l, int w, int nbits_n2, int path);
+PCMM_API int pcmm_paillier_mul(int path, const uint8_t *A_d, int m, int n, int l, int w, int iters,
+                               const uint32_t *N2_h, int nbits_n2, const uint32_t *ctB_d, uint32_t *ctC_d,
+                               void *ws_d, size_t ws_bytes, void *stream);
+
 /* ---- NEXT-2: fixed-base comb encryption ---------------
  * Encrypt with per-key precomputed tables: a context holds
  * T_P[i][v] = v 2^(8i) P for P in {G, H = pk}, 32 byte windows i, v < 256,

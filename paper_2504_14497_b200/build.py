@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpcmm.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-UNITS = ["hot.cu", "kernels.cu", "strassen.cu", "wide.cu", "next2.cu", "api.cu"]
+UNITS = ["hot.cu", "kernels.cu", "strassen.cu", "wide.cu", "next2.cu", "paillier.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", INCLUDE]
 

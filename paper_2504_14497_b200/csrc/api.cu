@@ -464,6 +464,69 @@ int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t coun
     return rc;
 }
 
+// ---------------------------------------------------------------- NEXT-4: Paillier
+static bool paillier_layout(int m, int n, int l, int w, int nbits, int path, size_t off[6], size_t *total, int *S,
+                            int *maxup) {
+    if (m <= 0 || n <= 0 || l <= 0 || w < 1 || w > 8 || (nbits % 32) != 0) return false;
+    const int L = nbits / 32;
+    if (!paillier_limbs_ok(L) || (path != 0 && path != 1)) return false;
+    if ((int64_t)m * l > (1LL << 30) || (int64_t)n * l > (1LL << 30)) return false;
+    *S = table_slots(w);
+    *maxup = max_upper(w);
+    size_t o = 256;
+    off[0] = o;
+    o = align256(o + (size_t)3 * L * 4);
+    off[1] = o;
+    o = align256(o + (size_t)n * l * L * 4);
+    off[2] = off[3] = off[4] = off[5] = o;
+    if (path == 1) {
+        off[2] = o;
+        o = align256(o + (size_t)n * sizeof(ColPlan));
+        off[3] = o;
+        o = align256(o + (size_t)n * m);
+        off[4] = o;
+        o = align256(o + (size_t)n * l * (*S) * L * 4);
+        off[5] = o;
+        o = align256(o + (size_t)n * l * 2 * (*maxup) * L * 4);
+    }
+    *total = o;
+    return true;
+}
+
+size_t pcmm_paillier_workspace_bytes(int m, int n, int l, int w, int nbits_n2, int path) {
+    size_t off[6], total = 0;
+    int S, maxup;
+    return paillier_layout(m, n, l, w, nbits_n2, path, off, &total, &S, &maxup) ? total : 0;
+}
+
+int pcmm_paillier_mul(int path, const uint8_t *A_d, int m, int n, int l, int w, int iters, const uint32_t *N2_h,
+                      int nbits_n2, const uint32_t *ctB_d, uint32_t *ctC_d, void *ws_d, size_t ws_bytes,
+                      void *stream) {
+    g_err.clear();
+    int rc = check_dims(m, n, l);
+    if (rc) return rc;
+    if (!A_d || !N2_h || !ctB_d || !ctC_d || !ws_d) return fail(PCMM_EINVAL, "null pointer");
+    if (((uintptr_t)ws_d & 255) || ((uintptr_t)ctB_d & 3) || ((uintptr_t)ctC_d & 3))
+        return fail(PCMM_EINVAL, "misaligned buffer (workspace 256 B, ciphertexts 4 B)");
+    if (path != 0 && path != 1) return fail(PCMM_EINVAL, "path must be 0 (schoolbook) or 1 (Cussen)");
+    if (w < 1 || w > 8) return fail(PCMM_EINVAL, "w must be in [1, 8]");
+    if (path == 1 && (iters < 1 || iters > 4)) return fail(PCMM_ENOTSUP, "iters must be in [1, 4]");
+    if (nbits_n2 % 32 || !paillier_limbs_ok(nbits_n2 / 32))
+        return fail(PCMM_ENOTSUP, "n^2 must have 512, 1024, 2048 or 3072 bits");
+    if (!(N2_h[0] & 1u)) return fail(PCMM_EINVAL, "n^2 must be odd");
+    size_t off[6], total = 0;
+    int S, maxup;
+    if (!paillier_layout(m, n, l, w, nbits_n2, path, off, &total, &S, &maxup))
+        return fail(PCMM_EDIM, "dimensions too large");
+    if (ws_bytes < total) return fail(PCMM_ENOMEM, "workspace too small (see pcmm_paillier_workspace_bytes)");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)ws_d;
+    CK(cudaMemsetAsync(ws, 0, 4, s), "memset status");
+    CK(run_paillier(path, A_d, m, n, l, w, iters, nbits_n2 / 32, N2_h, ctB_d, ctC_d, ws, off, S, maxup, s),
+       "paillier");
+    return PCMM_OK;
+}
+
 // ---------------------------------------------------------------- NEXT-2
 size_t pcmm_enc_ctx_bytes(void) { return enc_ctx_bytes(); }
 

@@ -73,6 +73,12 @@ int num_sms();
 cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w, int is_signed,
                          const uint32_t *bsoa, int leaf, uint32_t *out, int *status, cudaStream_t s);
 int accum_ctas_per_sm(int slots);
+// NEXT-4 (paillier.cu): PC-MM mod n^2, L 32-bit limbs; off[] = workspace offsets
+// {consts (one, R^2, unit: 3L words), Montgomery ciphertexts, plans, rank, tables, scratch}
+bool paillier_limbs_ok(int L);
+cudaError_t run_paillier(int path, const uint8_t *A, int m, int n, int l, int w, int N, int L, const uint32_t *Nh,
+                         const uint32_t *ctB, uint32_t *ctC, uint8_t *ws, const size_t *off, int S, int maxup,
+                         cudaStream_t s);
 // NEXT-2 (next2.cu): fixed-base comb encryption context, BSGS decryption context
 size_t enc_ctx_bytes();
 cudaError_t launch_enc_ctx_init(const uint8_t pk[64], uint32_t *ctx, cudaStream_t s);   // synchronises s

@@ -34,7 +34,7 @@ EXPORTS = [
     "pcmm_profile_enable", "pcmm_profile_read", "pcmm_test_field", "pcmm_test_point", "pcmm_test_plan",
     "pcmm_bench_fp_mul", "pcmm_workspace_bytes_wide", "pcmm_mul_cussen_wide", "pcmm_mul_schoolbook_wide",
     "pcmm_mul_strassen_wide", "pcmm_enc_ctx_bytes", "pcmm_enc_ctx_init", "pcmm_encrypt_ctx", "pcmm_bsgs_ctx_bytes",
-    "pcmm_bsgs_init", "pcmm_decrypt_bsgs",
+    "pcmm_bsgs_init", "pcmm_decrypt_bsgs", "pcmm_paillier_workspace_bytes", "pcmm_paillier_mul",
 ]
 
 
@@ -96,6 +96,9 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
             L.pcmm_bsgs_ctx_bytes.argtypes = [i32]
             L.pcmm_bsgs_init.argtypes = [i32, vp, vp]
             L.pcmm_decrypt_bsgs.argtypes = [vp, vp, i32, vp, i64, i64, i64, vp, vp, vp]
+            L.pcmm_paillier_workspace_bytes.restype = sz
+            L.pcmm_paillier_workspace_bytes.argtypes = [i32] * 6
+            L.pcmm_paillier_mul.argtypes = [i32, vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, sz, vp]
             _lib = L
     return _lib
 
@@ -210,6 +213,49 @@ def decrypt_bsgs(sk: bytes, ctx: torch.Tensor, log2_baby: int, ct: torch.Tensor,
     _check(load().pcmm_decrypt_bsgs(skb, _dev(ctx, torch.uint8, "ctx"), log2_baby, _dev(ct, torch.uint8, "ct"),
                                     count, lo, hi, m.data_ptr(), st.data_ptr(), _stream(stream)))
     return m, st
+
+
+# ------------------------------------------------------------------ NEXT-4: Paillier PC-MM
+def paillier_mul(path: int, A: torch.Tensor, ctB: torch.Tensor, l: int, w: int, n2: int, iters: int = 4,
+                 check: bool = True, stream=None) -> torch.Tensor:
+    """C_ij = prod_k c_kj^{a_ik} mod n^2 on the device.
+    A uint8 [m, n] (cuda), ctB int32 [n*l, L] little-endian words of residues < n2 (cuda),
+    n2 a Python int of 512 / 1024 / 2048 / 3072 bits.  Returns int32 [m*l, L] (same word layout)."""
+    _require_cuda()
+    m, n = A.shape
+    nbits = 32 * ctB.shape[-1]
+    if n2.bit_length() > nbits:
+        raise PCMMError(PCMM_EINVAL, "n2 does not fit the ciphertext width")
+    L = nbits // 32
+    words = (ctypes.c_uint32 * L)(*[(n2 >> (32 * i)) & 0xFFFFFFFF for i in range(L)])
+    nb = int(load().pcmm_paillier_workspace_bytes(m, n, l, w, nbits, path))
+    if nb == 0:
+        raise PCMMError(PCMM_EINVAL, "invalid Paillier PC-MM arguments")
+    ws = torch.empty(nb, dtype=torch.uint8, device=A.device)
+    out = torch.empty((m * l, L), dtype=torch.int32, device=A.device)
+    _check(load().pcmm_paillier_mul(path, _dev(A, torch.uint8, "A"), m, n, l, w, iters, words, nbits,
+                                    _dev(ctB, torch.int32, "ctB"), out.data_ptr(), ws.data_ptr(), nb,
+                                    _stream(stream)))
+    if check:
+        status(ws, stream)
+    return out
+
+
+def to_words(vals, L: int) -> torch.Tensor:
+    """Python ints -> int32 [len, L] little-endian 32-bit words (host tensor)."""
+    import numpy as np
+    a = np.zeros((len(vals), L), dtype=np.uint32)
+    for e, v in enumerate(vals):
+        for i in range(L):
+            a[e, i] = (v >> (32 * i)) & 0xFFFFFFFF
+    return torch.from_numpy(a.view(np.int32))
+
+
+def from_words(t: torch.Tensor) -> list:
+    """int32 [count, L] words -> Python ints."""
+    import numpy as np
+    a = t.cpu().numpy().view(np.uint32)
+    return [sum(int(a[e, i]) << (32 * i) for i in range(a.shape[1])) for e in range(a.shape[0])]
 
 
 # ------------------------------------------------------------------ PC-MM

@@ -58,6 +58,10 @@ def test_validation_without_gpu():
     assert L.pcmm_workspace_bytes_wide(4, 4, 4, 16, 1) > 0
     assert L.pcmm_workspace_bytes_wide(4, 4, 4, 17, 1) == 0
     assert L.pcmm_workspace_bytes_wide(16385, 4, 4, 16, 1) == 0
+    L.pcmm_paillier_workspace_bytes.restype = ctypes.c_size_t
+    assert L.pcmm_paillier_workspace_bytes(4, 4, 4, 4, 3072, 1) > 0
+    assert L.pcmm_paillier_workspace_bytes(4, 4, 4, 4, 4096, 1) == 0
+    assert L.pcmm_paillier_workspace_bytes(4, 4, 4, 9, 3072, 0) == 0
     rc = L.pcmm_mul_cussen(None, 0, 4, 4, 4, 0, 4, None, None, None, 0, None)
     assert rc == pcmm.PCMM_EDIM
     rc = L.pcmm_mul_cussen(None, 4, 4, 4, 4, 0, 4, None, None, None, 0, None)

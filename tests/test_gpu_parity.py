@@ -476,3 +476,47 @@ def test_pcmm_output_decrypts_with_bsgs():
     m, st = P.decrypt_bsgs(sk, bctx, 12, out, 0, 64 * 15 * 255)
     assert (st.cpu().numpy() == 0).all()
     assert (m.cpu().numpy().reshape(16, 8) == I.A.astype(np.int64) @ I.B.astype(np.int64)).all()
+
+
+# ------------------------------------------------------------------ NEXT-4: Paillier PC-MM
+@pytest.mark.parametrize("nbits,shape,w", [(512, (9, 7, 5), 4), (1024, (6, 10, 3), 8), (3072, (8, 8, 8), 4),
+                                           (2048, (5, 6, 4), 2)])
+def test_paillier_every_output(nbits, shape, w):
+    from oracle import paillier as pl
+    m, nn, l = shape
+    p, q = synth.paillier_primes(nbits, nbits // 2)
+    n, g, lam, mu = pl.keygen(p, q)
+    n2 = n * n
+    assert n2.bit_length() in (nbits, nbits - 1)
+    gen = synth.SplitMix64(nbits + w)
+    A = gen.small(0, (1 << w) - 1, m * nn).reshape(m, nn).astype(np.uint8)
+    A[0, :] = 0
+    A[1, 0] = (1 << w) - 1
+    A[2, :] = A[3, :]
+    B = gen.small(0, 255, nn * l).reshape(nn, l)
+    R = synth.paillier_random_units(nbits, n, nn * l)
+    C = [[pl.encrypt(n, g, int(B[k, j]), R[k * l + j]) for j in range(l)] for k in range(nn)]
+    exp = pl.pcmm_schoolbook(A, C, n2, w)
+    ct = P.to_words([C[k][j] for k in range(nn) for j in range(l)], nbits // 32).cuda()
+    for path in (P.SCHOOLBOOK, P.CUSSEN):
+        out = P.from_words(P.paillier_mul(path, cuda(A), ct, l, w, n2))
+        assert out == [exp[i][j] for i in range(m) for j in range(l)], path
+    AB = A.astype(np.int64) @ B.astype(np.int64)
+    assert pl.decrypt(n, lam, mu, out[0 * l + 1]) == AB[0, 1] == 0
+    assert pl.decrypt(n, lam, mu, out[4 * l + 2]) == AB[4, 2]
+
+
+def test_paillier_errors():
+    p, q = synth.paillier_primes(512, 256)
+    n2 = (p * q) ** 2
+    A = np.ones((2, 2), dtype=np.uint8)
+    ct = P.to_words([n2 - 1, 2, 3, n2 + 5 - n2], 16).cuda()
+    ok = P.paillier_mul(P.CUSSEN, cuda(A), ct, 2, 4, n2)
+    assert ok.shape == (4, 16)
+    bad = P.to_words([n2 + 1, 2, 3, 4], 16).cuda()            # a value >= n^2
+    with pytest.raises(P.PCMMError) as e:
+        P.paillier_mul(P.CUSSEN, cuda(A), bad, 2, 4, n2)
+    assert e.value.code == P.PCMM_ENOTONCURVE
+    with pytest.raises(P.PCMMError) as e:
+        P.paillier_mul(P.SCHOOLBOOK, cuda(np.full((2, 2), 16, dtype=np.uint8)), ct, 2, 4, n2)
+    assert e.value.code == P.PCMM_EBOUND
