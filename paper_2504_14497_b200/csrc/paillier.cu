@@ -114,17 +114,31 @@ __device__ void ladder(uint32_t *out, const uint32_t *g, int k, int t, const uin
     st<L>(out, x);
 }
 
-// key setup (one thread): R mod N and R^2 mod N by modular doubling of 1
+// key setup (one thread): R mod N = 2^(32L) - kN (at most 4 subtractions: N has
+// 32L - 1 or 32L bits), then x = 2^(L/2) R mod N by L/2 modular doublings and
+// six Montgomery squarings x <- x^2 R^-1: 2^((L/2) 64) R = R^2 mod N.
 template <int L>
 __global__ void k_pl_setup(const __grid_constant__ ModN<L> M, uint32_t *__restrict__ one, uint32_t *__restrict__ r2,
                            uint32_t *__restrict__ unit) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int j = 0; j < L; j++) unit[j] = j == 0 ? 1u : 0u;  // plain 1: mont_mul(x, 1) leaves Montgomery form
-    uint32_t x[L];
-    for (int j = 0; j < L; j++) x[j] = j == 0 ? 1u : 0u;
-    for (int it = 1; it <= 64 * L; it++) {
+    uint32_t x[L], top = 1;                                  // x + top 2^(32L) = 2^(32L)
+    for (int j = 0; j < L; j++) x[j] = 0;
+    for (int rep = 0; rep < 8; rep++) {                      // while (top, x) >= N: subtract N
+        uint32_t d[L], borrow = 0;
+        for (int j = 0; j < L; j++) {
+            const uint64_t v = (uint64_t)x[j] - M.n[j] - borrow;
+            d[j] = (uint32_t)v;
+            borrow = (uint32_t)(v >> 63);
+        }
+        if (top < borrow) break;                             // (top, x) < N
+        top -= borrow;
+        for (int j = 0; j < L; j++) x[j] = d[j];
+    }
+    for (int j = 0; j < L; j++) one[j] = x[j];
+    for (int it = 0; it < L / 2; it++) {                     // x <- 2x mod N
         uint32_t c = 0;
-        for (int j = 0; j < L; j++) {             // x <- 2x
+        for (int j = 0; j < L; j++) {
             const uint32_t nx = (x[j] << 1) | c;
             c = x[j] >> 31;
             x[j] = nx;
@@ -137,10 +151,12 @@ __global__ void k_pl_setup(const __grid_constant__ ModN<L> M, uint32_t *__restri
         }
         if (c || !borrow)
             for (int j = 0; j < L; j++) x[j] = d[j];
-        if (it == 32 * L)
-            for (int j = 0; j < L; j++) one[j] = x[j];
     }
-    for (int j = 0; j < L; j++) r2[j] = x[j];
+    for (int sq = 0; sq < 6; sq++) {
+        st<L>(r2, x);
+        mont_mul<L>(x, x, r2, M);
+    }
+    st<L>(r2, x);
 }
 
 // normal -> Montgomery form (c R mod N = mont_mul(c, R^2)); status bit if c >= N
