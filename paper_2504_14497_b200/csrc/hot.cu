@@ -25,6 +25,10 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 // each lane then walks ITS OWN nonzero entries of the chunk (a_ik = 0 adds the
 // identity and is skipped, R1), so a warp runs max-over-lanes of the
 // nonzero count instead of KCH additions (25% zeros at w = 2).
+#ifndef PCMM_ACCUM_MINB
+#define PCMM_ACCUM_MINB 5       // resident CTAs per SM the register allocation targets (4: 128 regs, 5: 96)
+#endif
+
 template <int S>
 struct AccumCfg {
     static constexpr int kRows = 128;
@@ -61,7 +65,7 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
 }
 
 template <int S>
-__global__ void __launch_bounds__(AccumCfg<S>::kRows, 4)
+__global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
             uint32_t *__restrict__ out, int64_t split_stride) {
     constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk;
