@@ -52,7 +52,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
     def compile_unit(u):
         obj = os.path.join(BUILD, u.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *FLAGS, "-c", os.path.join(CSRC, u), "-o", obj]
+        cmd = [nvcc, *ARCH, *FLAGS, *os.environ.get("PCMM_EXTRA_NVCC_FLAGS", "").split(), "-c",
+               os.path.join(CSRC, u), "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -450,6 +450,30 @@ struct fe3 {
     fe x, y, z;
 };
 
+struct fe4 {
+    fe x, y, z, w;
+};
+
+// (a b, c^2, d^2) in one out-of-line call
+__device__ __noinline__ fe3 fe_m1s2_call(const fe a, const fe b, const fe c, const fe d) {
+    fe3 r;
+    fe_mul_fast(r.x, a, b);
+    fe_sqr_fast(r.y, c);
+    fe_sqr_fast(r.z, d);
+    return r;
+}
+
+// (a b, c d, e^2, f^2) in one out-of-line call
+__device__ __noinline__ fe4 fe_m2s2_call(const fe a, const fe b, const fe c, const fe d, const fe e, const fe f) {
+    fe4 r;
+    fe_mul_fast(r.x, a, b);
+    fe_mul_fast(r.y, c, d);
+    fe_sqr_fast(r.z, e);
+    fe_sqr_fast(r.w, f);
+    return r;
+}
+
+
 // Three independent Montgomery products in one out-of-line call (the Jacobian
 // accumulate step has a stage with three independent products).
 __device__ __noinline__ fe3 fe_mul3_call(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
