@@ -201,6 +201,19 @@ cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w
            (n >> (D + 1)) >= leaf && (l >> (D + 1)) >= leaf)
         D++;
     cudaError_t err = cudaSuccess;
+    {
+        // keep the stream-ordered pool's memory mapped between calls: the per-level blocks are
+        // re-allocated every call, and returning them to the OS at each synchronisation made
+        // some calls 50x slower (measured in tools/grid.py)
+        static bool pool_tuned = false;
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (!pool_tuned && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            pool_tuned = true;
+        }
+    }
     auto note = [&](cudaError_t e) {
         if (err == cudaSuccess && e != cudaSuccess) err = e;
     };

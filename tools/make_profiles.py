@@ -70,6 +70,7 @@ def ncu_summary(rep, tag):
 launches()
 t_acc = ncu_summary(os.path.join(OUT, "prof_accum.ncu-rep"), "k_accum")
 t_tab = ncu_summary(os.path.join(OUT, "prof_tables.ncu-rep"), "k_tables")
+t_aff = ncu_summary(os.path.join(OUT, "prof_affine.ncu-rep"), "k_affine")
 tj = os.path.join(PROF, "traffic.json")
 data = json.load(open(tj)) if os.path.exists(tj) else {}
 data.setdefault("c256", {})
@@ -77,5 +78,7 @@ if t_acc:
     data["c256"]["accum_dram_bytes"] = t_acc
 if t_tab:
     data["c256"]["tables_dram_bytes"] = t_tab
+if t_aff:
+    data["c256"]["affine_dram_bytes"] = t_aff
 data["c256"]["source"] = f"ncu --set full capture ({rnd}), dram__bytes_read.sum + dram__bytes_write.sum per launch"
 json.dump(data, open(tj, "w"), indent=1)
