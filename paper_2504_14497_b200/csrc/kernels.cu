@@ -154,7 +154,10 @@ __device__ __forceinline__ void scr_load(pt &q, const uint32_t *scr, int64_t bas
     }
 }
 
-__global__ void __launch_bounds__(128, 3) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
+#ifndef PCMM_TABLES_MINB
+#define PCMM_TABLES_MINB 3
+#endif
+__global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
                                                    int n, int l, int N, int S, int maxup,
                                                    uint32_t *__restrict__ tables, uint32_t *__restrict__ scr) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
