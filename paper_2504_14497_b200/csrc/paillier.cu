@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(64) k_pl_tables(const __grid_constant__ ModN<L
                                                   uint32_t *__restrict__ tables, uint32_t *__restrict__ scr) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= (int64_t)n * l) return;
-    const int j = (int)(tid % l), k = (int)(tid / l);
+    const int k = (int)(tid / l);                            // tid = k l + j
     const ColPlan &pl = plans[k];
     const uint32_t *P = bm + tid * L;
     uint32_t *blk = tables + tid * (int64_t)S * L;
