@@ -67,3 +67,35 @@ def test_validation_without_gpu():
     rc = L.pcmm_mul_cussen(None, 4, 4, 4, 4, 0, 4, None, None, None, 0, None)
     assert rc == pcmm.PCMM_EINVAL
     assert L.pcmm_last_error()
+
+
+def test_validation_of_the_next_entry_points_without_gpu():
+    # NEXT-1 / NEXT-2 / NEXT-4 entry points reject bad arguments on the host, before any device work
+    from paper_2504_14497_b200 import pcmm
+    L = pcmm.load()
+    P = pcmm
+    # wide path: dimensions, null pointers, w range
+    assert L.pcmm_mul_cussen_wide(None, 0, 4, 4, 12, 0, 4, None, None, None, 0, None) == P.PCMM_EDIM
+    assert L.pcmm_mul_cussen_wide(None, 4, 4, 4, 12, 0, 4, None, None, None, 0, None) == P.PCMM_EINVAL
+    assert L.pcmm_mul_schoolbook_wide(None, 20000, 4, 4, 12, 0, None, None, None, 0, None) == P.PCMM_EDIM
+    assert L.pcmm_mul_strassen_wide(None, 4, 4, 4, 12, 0, 4, None, None, None, 0, None) == P.PCMM_EINVAL
+    # NEXT-2 contexts
+    assert L.pcmm_enc_ctx_bytes() == 256 + 2 * 32 * 256 * 64
+    assert L.pcmm_bsgs_ctx_bytes(0) == 0 and L.pcmm_bsgs_ctx_bytes(29) == 0
+    assert L.pcmm_bsgs_ctx_bytes(20) == 256 + (2 << 20) * 12
+    assert L.pcmm_enc_ctx_init(None, None, None) == P.PCMM_EINVAL
+    assert L.pcmm_encrypt_ctx(None, None, None, -1, None, None) == P.PCMM_EINVAL
+    assert L.pcmm_encrypt_ctx(None, None, None, 0, None, None) == P.PCMM_OK       # empty batch
+    assert L.pcmm_bsgs_init(0, None, None) == P.PCMM_EINVAL
+    assert L.pcmm_decrypt_bsgs(None, None, 20, None, 1, 5, 4, None, None, None) == P.PCMM_EINVAL   # hi < lo
+    assert L.pcmm_decrypt_bsgs(None, None, 4, None, 1, 0, 1 << 40, None, None, None) == P.PCMM_EINVAL  # range
+    assert L.pcmm_decrypt_bsgs(None, None, 20, None, 0, 0, 9, None, None, None) == P.PCMM_OK   # empty batch
+    # NEXT-4 Paillier
+    words = (ctypes.c_uint32 * 16)(*([3] + [0] * 15))
+    assert L.pcmm_paillier_mul(2, None, 4, 4, 4, 4, 4, words, 512, None, None, None, 0, None) == P.PCMM_EINVAL
+    assert L.pcmm_paillier_mul(1, None, 0, 4, 4, 4, 4, words, 512, None, None, None, 0, None) == P.PCMM_EDIM
+    even = (ctypes.c_uint32 * 16)(*([4] + [0] * 15))
+    p = ctypes.c_void_p(1 << 20)        # aligned, never dereferenced: validation fails first
+    assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 4, even, 512, p, p, p, 0, None) == P.PCMM_EINVAL
+    assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 4, words, 4096, p, p, p, 0, None) == P.PCMM_ENOTSUP
+    assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 5, words, 512, p, p, p, 0, None) == P.PCMM_ENOTSUP
