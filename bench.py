@@ -273,7 +273,7 @@ def main():
     out_h = torch.empty((count, 128), dtype=torch.uint8).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
+    def step(A=A, ctB=ctB, out=out):
         if path == P.CUSSEN:
             P.mul_cussen(A, ctB, l, w, cfg.signed, 4, out_proj=proj, ws=ws)
         elif path == P.STRASSEN:
@@ -281,6 +281,51 @@ def main():
         else:
             P.mul_schoolbook(A, ctB, l, w, cfg.signed, out_proj=proj, ws=ws)
         P.normalize(proj, count, out=out)
+
+    # pipelined end to end: two device input/output sets; the host->device copy of
+    # step k+1's inputs and the device->host copy of step k's result run on a copy
+    # stream while step k computes (every step still copies its own inputs and result)
+    copy_stream = torch.cuda.Stream(device=dev)
+    sets = [(A, ctB, out, out_h), (torch.empty_like(A), torch.empty_like(ctB), torch.empty_like(out),
+                                   torch.empty_like(out_h).pin_memory())]
+
+    def e2e_pipelined(K):
+        h2d = [torch.cuda.Event() for _ in range(2)]
+        comp = [torch.cuda.Event() for _ in range(2)]
+        d2h = [torch.cuda.Event() for _ in range(2)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(copy_stream)
+        with torch.cuda.stream(copy_stream):
+            sets[0][0].copy_(A_h, non_blocking=True)
+            sets[0][1].copy_(ctB_h, non_blocking=True)
+        h2d[0].record(copy_stream)
+        for k in range(K):
+            a_d, c_d, o_d, o_h = sets[k % 2]
+            stream.wait_event(h2d[k % 2])
+            if k >= 2:
+                stream.wait_event(d2h[k % 2])          # the result buffer of step k-2 has been read
+            step(a_d, c_d, o_d)
+            comp[k % 2].record(stream)
+            if k + 1 < K:
+                nxt = sets[(k + 1) % 2]
+                if k >= 1:
+                    copy_stream.wait_event(comp[(k + 1) % 2])   # step k-1 no longer reads that set
+                with torch.cuda.stream(copy_stream):
+                    nxt[0].copy_(A_h, non_blocking=True)
+                    nxt[1].copy_(ctB_h, non_blocking=True)
+                h2d[(k + 1) % 2].record(copy_stream)
+            copy_stream.wait_event(comp[k % 2])
+            with torch.cuda.stream(copy_stream):
+                o_h.copy_(o_d, non_blocking=True)
+            d2h[k % 2].record(copy_stream)
+        t1.record(copy_stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return reduce_max(t0.elapsed_time(t1) / K, dist, dev)
 
     def step_e2e():
         A.copy_(A_h, non_blocking=True)
@@ -317,8 +362,12 @@ def main():
         ms, prof = timed(step, args.steps, profile=True)
     clocks = clk.summary()
     P.status(ws)
-    ms_e2e, _ = timed(step_e2e, max(3, args.steps // 2))
+    ms_e2e_serial, _ = timed(step_e2e, max(3, args.steps // 2))
     P.status(ws)
+    e2e_pipelined(2)
+    ms_e2e = e2e_pipelined(max(3, args.steps // 2))
+    P.status(ws)
+    assert torch.equal(sets[1][3], out_h), "pipelined e2e results differ"
 
     # ---- kernel breakdown and roofline of the dominant kernel ----
     per = {}
@@ -368,7 +417,11 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": {"value": world * count / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
-                "h2d_bytes_per_step": int(A.numel() + ctB.numel()), "d2h_bytes_per_step": int(out.numel())},
+                "h2d_bytes_per_step": int(A.numel() + ctB.numel()), "d2h_bytes_per_step": int(out.numel()),
+                "mode": "pipelined: step k+1's H2D and step k's D2H on a copy stream overlap step k's compute "
+                        "(pinned host buffers, two device buffer sets, continuous timed region over all steps)",
+                "serial_ms_per_step": ms_e2e_serial,
+                "serial_value": world * count / (ms_e2e_serial * 1e-3)},
     }
     if path == P.CUSSEN and not args.no_schoolbook:
         def sb():
