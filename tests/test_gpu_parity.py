@@ -520,3 +520,34 @@ def test_paillier_errors():
     with pytest.raises(P.PCMMError) as e:
         P.paillier_mul(P.SCHOOLBOOK, cuda(np.full((2, 2), 16, dtype=np.uint8)), ct, 2, 4, n2)
     assert e.value.code == P.PCMM_EBOUND
+
+
+def test_wide_full_grid_size_sampled():
+    # the grid's 256^3 t = 16 run (tools/grid.py), in the launch configuration bench.py uses
+    # (default 2 GiB table budget -> several k-chunks): sampled outputs vs the Eq. 5 closed form
+    cfg = synth.Config("w16", 256, 256, 256, 16, False, 0, 255, 1616)
+    I = synth.make_instance(cfg)
+    sk, pk = P.keygen(cfg.seed)
+    ctd = P.encrypt(pk, cuda(I.B.reshape(-1).astype(np.int32)), cuda(I.r_be))
+    out = P.pcmm(cuda(I.A), ctd, 256, 16, False, path=P.CUSSEN).cpu().numpy()
+    r = I.r_be.reshape(256, 256, 32)
+    g = np.random.default_rng(16)
+    for (i, j) in [(0, 0), (255, 255)] + [(int(g.integers(256)), int(g.integers(256))) for _ in range(6)]:
+        assert out[i * 256 + j].tobytes() == oracle.closed_form(I.x, I.A[i], I.B[:, j], r[:, j]), (i, j)
+
+
+def test_paillier_3072_64cube_sampled():
+    # 64^3, t = 4, n^2 of 3072 bits, random residues mod n^2 as ciphertexts (any unit is the
+    # encryption of some message): sampled outputs vs the oracle's definition prod_k c^a mod n^2
+    from oracle import paillier as pl
+    p, q = synth.paillier_primes(3072, 1536)
+    n2 = (p * q) ** 2
+    g = synth.SplitMix64(64)
+    A = g.small(0, 15, 64 * 64).reshape(64, 64).astype(np.uint8)
+    vals = [pow(int(v), 5, n2) for v in g.small(2, 2**62, 64 * 64)]
+    ct = P.to_words(vals, 96).cuda()
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        out = P.from_words(P.paillier_mul(path, cuda(A), ct, 64, 4, n2))
+        for (i, j) in [(0, 0), (63, 63), (17, 5), (40, 33)]:
+            C = [[vals[k * 64 + j]] for k in range(64)]
+            assert out[i * 64 + j] == pl.pcmm_schoolbook(A[i:i + 1], C, n2, 4)[0][0], (path, i, j)
