@@ -82,6 +82,10 @@ Layout layout(int m, int n, int l, int w, int path) {
             const double cost = waves / cand * (1.0 + 0.01 * (cand - 1)) + (n / cand < 8 ? 1.0 : 0.0);
             if (cost < best - 1e-9) { best = cost; ks = cand; }
         }
+        if (const char *e = getenv("PCMM_KSPLIT")) {         // measurement override (tools/)
+            const int v = atoi(e);
+            if (v >= 1 && v <= n) ks = v;
+        }
         L.ksplit = ks;
         L.plans = off;
         off = align256(off + (size_t)n * sizeof(ColPlan));
