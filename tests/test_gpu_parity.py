@@ -551,3 +551,16 @@ def test_paillier_3072_64cube_sampled():
         for (i, j) in [(0, 0), (63, 63), (17, 5), (40, 33)]:
             C = [[vals[k * 64 + j]] for k in range(64)]
             assert out[i * 64 + j] == pl.pcmm_schoolbook(A[i:i + 1], C, n2, 4)[0][0], (path, i, j)
+
+
+@pytest.mark.parametrize("t", [4, 12])
+def test_vector_times_ciphertext_scalars(t):
+    # NEXT-1's vector workload (Tables A7/A8): an n x 1 plaintext vector times a 1 x l row of ciphertexts
+    m, l = 37, 5
+    cfg = synth.Config("vec", m, 1, l, t, False, 0, 255, 900 + t)
+    I = synth.make_instance(cfg)
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, l, t)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(I.A, ct, l, t, False, path) == exp).all(), path
