@@ -10,7 +10,8 @@ using namespace pcmm;
 
 extern "C" {
 
-// op: 0 add, 1 sub, 2 mul (plain a*b mod p via Montgomery), 3 inv, 4 neg
+// op: 0 add, 1 sub, 2 mul (plain a*b mod p via Montgomery), 3 inv (divsteps), 4 neg,
+//     5 inv (Fermat chain)
 int hfp_op(int op, const uint8_t *a_be, const uint8_t *b_be, uint8_t *out_be) {
     fe a, b, r;
     fe_from_be_bytes(a, a_be);
@@ -23,6 +24,7 @@ int hfp_op(int op, const uint8_t *a_be, const uint8_t *b_be, uint8_t *out_be) {
         case 2: fe_mul(r, a, b); break;
         case 3: fe_inv(r, a); break;
         case 4: fe_neg(r, a); break;
+        case 5: fe_inv_fermat(r, a); break;
         default: return -1;
     }
     fe_from_mont(r, r);

@@ -53,10 +53,11 @@ def test_field_ops_bit_exact():
         out = P.test_field(op, A, B).cpu().numpy()
         for i in range(len(a)):
             assert int.from_bytes(out[i].tobytes(), "big") == f(a[i], b[i]), (op, i)
-    out = P.test_field(3, A, B).cpu().numpy()
-    for i in range(len(a)):
-        exp = pow(a[i], -1, ecref.P) if a[i] else 0
-        assert int.from_bytes(out[i].tobytes(), "big") == exp
+    for op in (3, 7):                                       # divsteps, Fermat
+        out = P.test_field(op, A, B).cpu().numpy()
+        for i in range(len(a)):
+            exp = pow(a[i], -1, ecref.P) if a[i] else 0
+            assert int.from_bytes(out[i].tobytes(), "big") == exp, (op, i)
 
 
 def _pts(scalars):

@@ -53,7 +53,8 @@ def call(fn, *args, n=32):
 
 def test_field_ops_vs_python_ints():
     P = ecref.P
-    vals = [0, 1, 2, P - 1, P - 2, 2**224, 2**192 - 1, 2**96, 2**255 % P] + [rng.randrange(P) for _ in range(200)]
+    vals = [0, 1, 2, 3, P - 1, P - 2, P - 3, 2**224, 2**192 - 1, 2**96, 2**255 % P, 2**30, 2**30 - 1, 2**60 + 1,
+            (P + 1) // 2, P // 3] + [rng.randrange(P) for _ in range(600)] + [rng.randrange(2**40) for _ in range(50)]
     for a in vals:
         b = rng.choice(vals)
         get = lambda op: int.from_bytes(call(lib().hfp_op, op, b32(a), b32(b)), "big")
@@ -62,7 +63,10 @@ def test_field_ops_vs_python_ints():
         assert get(2) == (a * b) % P
         assert get(4) == (-a) % P
         if a:
-            assert get(3) == pow(a, -1, P)
+            assert get(3) == pow(a, -1, P)                 # divsteps (Bernstein-Yang)
+            assert get(5) == pow(a, -1, P)                 # Fermat chain
+        else:
+            assert get(3) == 0 and get(5) == 0
 
 
 def test_montgomery_raw_bound():
