@@ -696,7 +696,10 @@ cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int i
 
 cudaError_t launch_normalize(const uint32_t *proj, int64_t count, uint8_t *ct, cudaStream_t s) {
     if (count == 0) return cudaSuccess;
-    const int64_t threads = (2 * count + kBatch - 1) / kBatch;
+    // points per thread: up to kBatch (one inversion per batch), fewer when that would
+    // leave fewer than ~8 warps per SM (small outputs: the inversion latency is the cost)
+    const int64_t batch = std::min<int64_t>(kBatch, std::max<int64_t>(1, 2 * count / ((int64_t)num_sms() * 256)));
+    const int64_t threads = (2 * count + batch - 1) / batch;
     k_normalize<<<blocks_for(threads, 128), 128, 0, s>>>(proj, count, ct);
     return cudaGetLastError();
 }
