@@ -294,7 +294,8 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint8_t *rank = ws + L.rank;
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
-    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, tables, (uint32_t *)(ws + L.scratch), s));
+    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, is_signed, tables,
+                                            (uint32_t *)(ws + L.scratch), s));
     uint32_t *atables = (uint32_t *)(ws + L.scratch);
     LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s));
     const int64_t cnt = (int64_t)m * l;

@@ -39,7 +39,7 @@ cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s);
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          uint32_t *tables, uint32_t *scratch, cudaStream_t s);
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s);
 // homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s);
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of

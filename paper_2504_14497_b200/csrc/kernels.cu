@@ -154,9 +154,37 @@ __device__ __forceinline__ void scr_load(pt &q, const uint32_t *scr, int64_t bas
     }
 }
 
+// Alg. 3 line 5 for signed columns (k_tables<true>): v P for the level-N values
+// sN[0..cnt) (ascending) into upper-level scratch.  A value whose magnitude equals
+// the previous one's, or exceeds it by 1, reuses the previous product (|v| P =
+// |v'| P or |v'| P + P, then the sign): the ML columns' {-8, 8, 9} cost 3 doublings
+// + 1 addition instead of 9 + 1.  Out of line and only in the signed kernel: in
+// the unsigned kernel (s^(N) = {1} in practice) it cost registers for nothing.
+__device__ __noinline__ void level_n_products_shared(const int16_t *sN, int cnt, const pt P, uint32_t *sj,
+                                                     int64_t sbase, int64_t l, int src) {
+    pt prevabs, e;
+    int prevmag = -1;
+    for (int u = 0; u < cnt; u++) {
+        const int v = sN[u];
+        const int mag = v < 0 ? -v : v;
+        if (mag == prevmag) {
+            e = prevabs;
+        } else if (prevmag > 0 && mag == prevmag + 1) {
+            pt_add_pair(e, prevabs, P);
+        } else {
+            pt_mul_small_g<MulCall>(e, mag, P);
+        }
+        prevabs = e;
+        prevmag = mag;
+        if (v < 0) pt_neg(e, e);
+        scr_store(sj, sbase, src + u, l, e);
+    }
+}
+
 #ifndef PCMM_TABLES_MINB
 #define PCMM_TABLES_MINB 3
 #endif
+template <bool kSigned>
 __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
                                                    int n, int l, int N, int S, int maxup,
                                                    uint32_t *__restrict__ tables, uint32_t *__restrict__ scr) {
@@ -187,10 +215,14 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
         // level N (Alg. 3 line 5): buffer A = entries [0, 8), buffer B = [8, 16)
         int src = 0;
         const int nN = pl.n[N - 1];
-        for (int u = 0; u < nN; u++) {
-            pt e;
-            pt_mul_small_g<MulCall>(e, pl.sN[u], P);
-            scr_store(sj, sbase, src + u, l, e);
+        if (kSigned) {
+            level_n_products_shared(pl.sN, nN, P, sj, sbase, l, src);
+        } else {
+            for (int u = 0; u < nN; u++) {
+                pt e;
+                pt_mul_small_g<MulCall>(e, pl.sN[u], P);
+                scr_store(sj, sbase, src + u, l, e);
+            }
         }
         for (int lev = N - 1; lev >= 2; lev--) {                            // prefix sums, levels N-1 .. 2
             const int dst = maxup - src;
@@ -677,8 +709,11 @@ cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *ata
 }
 
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
-    k_tables<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
+    if (is_signed)
+        k_tables<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+    else
+        k_tables<false><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
     return cudaGetLastError();
 }
 
