@@ -25,6 +25,9 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 // each lane then walks ITS OWN nonzero entries of the chunk (a_ik = 0 adds the
 // identity and is skipped, R1), so a warp runs max-over-lanes of the
 // nonzero count instead of KCH additions (25% zeros at w = 2).
+#ifndef PCMM_ACCUM_CHUNK_SLOTS
+#define PCMM_ACCUM_CHUNK_SLOTS 512  // table slots staged per chunk: k-chunk = this / 2^w (32 at w = 4)
+#endif
 #ifndef PCMM_ACCUM_MINB
 #define PCMM_ACCUM_MINB 5       // resident CTAs per SM the register allocation targets (4: 128 regs, 5: 96)
 #endif
@@ -32,7 +35,7 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 template <int S>
 struct AccumCfg {
     static constexpr int kRows = 128;
-    static constexpr int kChunk = (512 / S) < 128 ? (512 / S) : 128;
+    static constexpr int kChunk = (PCMM_ACCUM_CHUNK_SLOTS / S) < 128 ? (PCMM_ACCUM_CHUNK_SLOTS / S) : 128;
     static constexpr int kTW = kAffWords * S;                      // words per table (global, entry-major)
     static constexpr int kEW = kAffWords + 1;                      // shared-memory entry stride (odd: no conflicts)
     static constexpr int kTWs = kEW * S;                           // words per table in shared memory
