@@ -565,3 +565,30 @@ def test_vector_times_ciphertext_scalars(t):
     exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, l, t)
     for path in (P.CUSSEN, P.SCHOOLBOOK):
         assert (_gpu_pcmm(I.A, ct, l, t, False, path) == exp).all(), path
+
+
+def test_step_is_cuda_graph_capturable():
+    # the Cussen step (mul + normalize) is stream-ordered with no host synchronisation, so it can be
+    # captured once into a CUDA graph and replayed (serving-style launch-overhead removal)
+    I = synth.make_instance(synth.CONFIGS["c64"], m=32, n=48, l=16, seed=41)
+    x = synth.keygen_secret(41)
+    ct = cuda(oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be))
+    A = cuda(I.A)
+    ref = P.pcmm(A, ct, 16, 4, False, P.CUSSEN).cpu()
+    ws = P.alloc_workspace(32, 48, 16, 4, P.CUSSEN)
+    proj = torch.empty(P.proj_bytes(32 * 16), dtype=torch.uint8, device="cuda")
+    out = torch.empty((32 * 16, 128), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):                       # warm-up outside capture (first-call attribute setup)
+        P.mul_cussen(A, ct, 16, 4, False, 4, out_proj=proj, ws=ws)
+        P.normalize(proj, 32 * 16, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        P.mul_cussen(A, ct, 16, 4, False, 4, out_proj=proj, ws=ws)
+        P.normalize(proj, 32 * 16, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), ref)
+    P.status(ws)
