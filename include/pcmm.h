@@ -264,8 +264,9 @@ PCMM_API int pcmm_profile_read(char *names_h, float *ms_h, int max);
  * (all mod p).  out_d[count][32].                                          */
 PCMM_API int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out_d, int64_t count, void *stream);
 /* Batched group ops on 64-byte canonical points: op 0 P+Q, 1 2P, 2 v*P
- * (v_d[e], |v| < 2^15), 3 k*P (k = 32-byte BE scalar in q_d[e][0..31]).
- * out_d[count][64].                                                          */
+ * (v_d[e], |v| < 2^15), 3 k*P (k = 32-byte BE scalar in q_d[e][0..31]; 4-bit
+ * windows, Jacobian: the encrypt / decrypt ECSM), 4 k*P (binary double-and-
+ * add with the complete formulas).  out_d[count][64].                        */
 PCMM_API int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_t *v_d, uint8_t *out_d,
                     int64_t count, void *stream);
 /* The device compression plan of Alg. 2 (step a1) for every column of A:

@@ -653,7 +653,7 @@ int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out
 int pcmm_test_point(int op, const uint8_t *p_d, const uint8_t *q_d, const int32_t *v_d, uint8_t *out_d,
                     int64_t count, void *stream) {
     g_err.clear();
-    if (count < 0 || op < 0 || op > 3) return fail(PCMM_EINVAL, "bad op / count");
+    if (count < 0 || op < 0 || op > 4) return fail(PCMM_EINVAL, "bad op / count");
     if (count && (!p_d || !out_d || ((op == 0 || op == 3) && !q_d) || (op == 2 && !v_d)))
         return fail(PCMM_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)stream;

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "canon.cuh"
+#include "jac.cuh"
 #include "ec.cuh"
 #include "internal.h"
 
@@ -528,8 +529,8 @@ __global__ void k_encrypt(const __grid_constant__ Pk64 pk, const int32_t *__rest
     pt_from_canonical(H, pkb);
     uint32_t k[8];
     be32_to_words(r + e * 32, k);
-    pt_mul_scalar(C1, k, G);                  // r G
-    pt_mul_scalar(C2, k, H);                  // r H
+    pt_mul_scalar_win(C1, k, G);              // r G
+    pt_mul_scalar_win(C2, k, H);              // r H
     pt_mul_small(bG, bvals[e], G);            // phi(b) = b G
     pt_add_nl(C2, C2, bG);
     store_canonical_point(ct + e * 128, C1);
@@ -583,7 +584,7 @@ __global__ void k_decrypt(const __grid_constant__ Scalar8 x, const uint8_t *__re
     uint32_t xk[8];                            // local copy (never index the param space)
 #pragma unroll
     for (int i = 0; i < 8; i++) xk[i] = x.k[i];
-    pt_mul_scalar(M, xk, C1);
+    pt_mul_scalar_win(M, xk, C1);             // C1 decoded: Z = 1 or the identity
     pt_neg(M, M);
     pt_add_nl(M, C2, M);                        // C2 - x C1 = phi(m)
     __align__(16) uint8_t buf[64];
@@ -656,10 +657,14 @@ __global__ void k_test_point(int op, const uint8_t *__restrict__ p, const uint8_
         pt_dbl_nl(R, P);
     } else if (op == 2) {
         pt_mul_small(R, v[e], P);
+    } else if (op == 3) {
+        uint32_t k[8];
+        be32_to_words(q + e * 64, k);
+        pt_mul_scalar_win(R, k, P);           // 4-bit windows, Jacobian (the decrypt / encrypt ECSM)
     } else {
         uint32_t k[8];
         be32_to_words(q + e * 64, k);
-        pt_mul_scalar(R, k, P);
+        pt_mul_scalar(R, k, P);               // binary double-and-add, complete formulas
     }
     store_canonical_point(out + e * 64, R);
 }

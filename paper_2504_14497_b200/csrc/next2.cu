@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(64) k_decrypt_bsgs(const __grid_constant__ Sc8
     uint32_t xk[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) xk[i] = xs.k[i];
-    pt_mul_scalar(M, xk, C1);
+    pt_mul_scalar_win(M, xk, C1);                         // C1 decoded: Z = 1 or the identity
     pt_neg(M, M);
     pt_add_nl(M, C2, M);                                  // C2 - x C1 = phi(m)
 #pragma unroll

@@ -77,8 +77,11 @@ def test_point_ops_vs_openssl():
     v[4], v[5] = 0, 1
     mul = P.test_point(2, Pa, v=cuda(np.array(v, dtype=np.int32))).cpu().numpy()
     k = [rng.randrange(2**256) for _ in range(n)]
+    k[6], k[7], k[8], k[9] = 0, 1, 15, 2**256 - 1          # empty, single, one-window and all-ones scalars
     K = cuda(np.frombuffer(b"".join(x.to_bytes(32, "big") + bytes(32) for x in k), dtype=np.uint8).reshape(-1, 64))
     kmul = P.test_point(3, Pa, K).cpu().numpy()
+    kmul2 = P.test_point(4, Pa, K).cpu().numpy()
+    assert (kmul == kmul2).all()
     for i in range(n):
         assert add[i].tobytes() == ecref.mulG(a[i] + b[i]), i
         assert dbl[i].tobytes() == ecref.mulG(2 * a[i]), i

@@ -38,7 +38,7 @@ t_ctx = (time.time() - t0) * 1e3
 ms_l = timed(lambda: P.encrypt(pk, b, r))
 ms_c = timed(lambda: P.encrypt_ctx(ctx, b, r))
 assert (P.encrypt(pk, b, r) == P.encrypt_ctx(ctx, b, r)).all()
-rows.append(f"| encrypt 65,536 | 2 x 256-bit double-and-add (pcmm_encrypt) | {ms_l:.3f} | {count / ms_l * 1e3:,.0f} |")
+rows.append(f"| encrypt 65,536 | two 256-bit 4-bit-window ECSMs (pcmm_encrypt) | {ms_l:.3f} | {count / ms_l * 1e3:,.0f} |")
 rows.append(f"| encrypt 65,536 | comb context (pcmm_encrypt_ctx) | {ms_c:.3f} | {count / ms_c * 1e3:,.0f} |")
 rows.append(f"| comb context build (once per key, wall) | pcmm_enc_ctx_init | {t_ctx:.1f} | |")
 ct = P.encrypt_ctx(ctx, b, r)
