@@ -450,6 +450,20 @@ struct fe3 {
     fe x, y, z;
 };
 
+// The accumulate step's product groups (jac.cuh jac_add_aff).  Inlined by default
+// (PCMM_INLINE_ACCUM=1): with the even/odd product the whole step is ~40 KB of
+// SASS, just past the 32 KB L1.5 instruction cache, and the call glue (argument
+// moves on the FMA-heavy pipe) costs more than the misses: measured at 4 CTAs per
+// SM, 256^3 / 512^3 / ML accumulate 1.7 / 4.9 / 4.3 % faster than out of line.
+#ifndef PCMM_INLINE_ACCUM
+#define PCMM_INLINE_ACCUM 1
+#endif
+#if PCMM_INLINE_ACCUM
+#define PCMM_HOTCALL __forceinline__
+#else
+#define PCMM_HOTCALL __noinline__
+#endif
+
 struct fe4 {
     fe x, y, z, w;
 };
@@ -478,6 +492,33 @@ __device__ __noinline__ fe4 fe_m2s2_call(const fe a, const fe b, const fe c, con
 // accumulate step has a stage with three independent products).
 __device__ __noinline__ fe3 fe_mul3_call(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
                                          const fe b2) {
+    fe3 r;
+    fe_mul_fast(r.x, a0, b0);
+    fe_mul_fast(r.y, a1, b1);
+    fe_mul_fast(r.z, a2, b2);
+    return r;
+}
+
+}  // namespace pcmm
+
+namespace pcmm {
+
+__device__ PCMM_HOTCALL fe2 fe_mul2_hot(const fe a0, const fe b0, const fe a1, const fe b1) {
+    fe2 r;
+    fe_mul_fast(r.x, a0, b0);
+    fe_mul_fast(r.y, a1, b1);
+    return r;
+}
+
+__device__ PCMM_HOTCALL fe2 fe_mulsqr_hot(const fe a, const fe b, const fe c) {
+    fe2 r;
+    fe_mul_fast(r.x, a, b);
+    fe_sqr_fast(r.y, c);
+    return r;
+}
+
+__device__ PCMM_HOTCALL fe3 fe_mul3_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
+                                        const fe b2) {
     fe3 r;
     fe_mul_fast(r.x, a0, b0);
     fe_mul_fast(r.y, a1, b1);

@@ -29,7 +29,7 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #define PCMM_ACCUM_CHUNK_SLOTS 512  // table slots staged per chunk: k-chunk = this / 2^w (32 at w = 4)
 #endif
 #ifndef PCMM_ACCUM_MINB
-#define PCMM_ACCUM_MINB 5       // resident CTAs per SM the register allocation targets (4: 128 regs, 5: 96)
+#define PCMM_ACCUM_MINB 4       // resident CTAs per SM the register allocation targets (4: 128 regs, 5: 96)
 #endif
 
 template <int S>

@@ -70,8 +70,8 @@ __device__ __forceinline__ void jac_add_aff(jacc &A, const fe &x2, const fe &y2)
         A = jac_add_slow(A, x2, y2);
         return;
     }
-    fe U2, T1;
-    mul2(U2, x2, A.ZZ, T1, A.Z, A.ZZ);            // U2 = x2 ZZ, T1 = Z^3
+    const fe2 ut = fe_mul2_hot(x2, A.ZZ, A.Z, A.ZZ);   // U2 = x2 ZZ, T1 = Z^3
+    const fe &U2 = ut.x, &T1 = ut.y;
     fe H;
     fe_sub(H, U2, A.X);
     if (fe_is_zero(H)) {
@@ -79,21 +79,20 @@ __device__ __forceinline__ void jac_add_aff(jacc &A, const fe &x2, const fe &y2)
         return;
     }
 #if PCMM_JAC_FORMULA == 1
-    const fe2 sh = fe_mulsqr_call(y2, T1, H);     // S2 = y2 Z^3, HH = H^2
+    const fe2 sh = fe_mulsqr_hot(y2, T1, H);     // S2 = y2 Z^3, HH = H^2
     const fe &S2 = sh.x, &HH = sh.y;
     fe R;
     fe_sub(R, S2, A.Y);
-    const fe3 t = fe_mul3_call(H, HH, A.X, HH, A.ZZ, HH);  // H^3, V = X1 H^2, ZZ3
-    const fe2 zr = fe_mulsqr_call(A.Z, H, R);     // Z3 = Z1 H, R^2
+    const fe3 t = fe_mul3_hot(H, HH, A.X, HH, A.ZZ, HH);  // H^3, V = X1 H^2, ZZ3
+    const fe2 zr = fe_mulsqr_hot(A.Z, H, R);     // Z3 = Z1 H, R^2
     const fe &Z3 = zr.x, &R2 = zr.y;
     fe X3, V2, D;
     fe_add(V2, t.y, t.y);
     fe_sub(X3, R2, t.x);
     fe_sub(X3, X3, V2);                           // X3 = R^2 - H^3 - 2V
     fe_sub(D, t.y, X3);
-    fe Y3a, YH;
-    mul2(Y3a, R, D, YH, A.Y, t.x);                // R (V - X3), Y1 H^3
-    fe_sub(A.Y, Y3a, YH);
+    const fe2 yy = fe_mul2_hot(R, D, A.Y, t.x);   // R (V - X3), Y1 H^3
+    fe_sub(A.Y, yy.x, yy.y);
     A.X = X3;
     A.Z = Z3;
     A.ZZ = t.z;
