@@ -39,10 +39,10 @@ UNIT = "entries/s"
 P_PROD = 32.0
 LIMB_PRODUCTS_PER_FPMUL = 64.0
 FPMUL_PER_ADD = 14          # RCB16 Alg. 4: 12M + 2 m_b (table build)
-# k_accum: Jacobian + affine mixed addition 8M + 3S; the two squares of the hot loop
-# (H^2, R^2) run through the 36-product squaring, Z^2 is carried as a product:
-# 9 products + 2 x 36/64 = 10.125 fp_mul-equivalents of IMAD work per addition
-FPMUL_PER_ACC_ADD = 9 + 2 * 36 / 64
+# k_accum: XYZZ + affine mixed addition (madd-2008-s) 8M + 2S; the two squares of
+# the hot loop (P^2, R^2) run through the 36-product squaring:
+# 8 products + 2 x 36/64 = 9.125 fp_mul-equivalents of IMAD work per addition
+FPMUL_PER_ACC_ADD = 8 + 2 * 36 / 64
 FPMUL_PER_AFFINE = 6        # k_affine: 5 products per table entry + the warp-shared inversion (amortised)
 FPMUL_PER_DBL = 13          # RCB16 Alg. 6: 8M + 3S + 2 m_b
 FPMUL_PER_NORM = 6          # batch inversion + x, y + from-Montgomery (amortised)
@@ -418,7 +418,7 @@ def main():
                 "unit": "G fp_mul/s", "frac": achieved / peak_fpmul, "traffic": traffic,
                 "peak_note": f"{nsm} SM x {P_PROD:.0f} 32x32->64 products/clk/SM x {f_max / 1e9:.3f} GHz (sm_max) "
                              f"/ 64 products per fp_mul; IMAD.WIDE half-rate measured by tools/k11_imad_probe.cu",
-                "algorithmic": f"{FPMUL_PER_ACC_ADD} fp_mul-equivalents (8M + 3S Jacobian + affine; squares at "
+                "algorithmic": f"{FPMUL_PER_ACC_ADD} fp_mul-equivalents (8M + 2S XYZZ + affine; squares at "
                                f"36/64) x {acc_adds} useful "
                                f"accumulate adds (a_ik != 0)"}
 

@@ -517,6 +517,13 @@ __device__ PCMM_HOTCALL fe2 fe_mulsqr_hot(const fe a, const fe b, const fe c) {
     return r;
 }
 
+__device__ PCMM_HOTCALL fe2 fe_sqr2_hot(const fe a, const fe b) {
+    fe2 r;
+    fe_sqr_fast(r.x, a);
+    fe_sqr_fast(r.y, b);
+    return r;
+}
+
 __device__ PCMM_HOTCALL fe3 fe_mul3_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
                                         const fe b2) {
     fe3 r;

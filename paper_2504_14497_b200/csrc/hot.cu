@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
     const int tid = (int)threadIdx.x;
     const int i = rb * ROWS + tid;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
-    jacc acc;
-    jac_init(acc);
+    acc_t acc;
+    acc_init(acc);
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
                 x2.v[q] = T[q];
                 y2.v[q] = T[8 + q];
             }
-            jac_add_aff(acc, x2, y2);
+            acc_add_aff(acc, x2, y2);
             kk++;
             while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
         }
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
     if (i < m) {
         const int64_t cnt = (int64_t)m * l;
         pt o;
-        jac_to_proj(o, acc);
+        acc_to_proj(o, acc);
         soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
     }
 }
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kRowsG, 3)
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
     const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive k
     const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kAffWords;
-    jacc acc;
-    jac_init(acc);
+    acc_t acc;
+    acc_init(acc);
     int k = kb;
     while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
     if (k < ke) {
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
             while (kn < ke && rank[(int64_t)kn * m + i] == 0) kn++;
             fe xn, yn;
             if (kn < ke) load_aff(xn, yn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kAffWords);
-            jac_add_aff(acc, x2, y2);
+            acc_add_aff(acc, x2, y2);
             if (kn >= ke) break;
             x2 = xn;
             y2 = yn;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
     }
     const int64_t cnt = (int64_t)m * l;
     pt o;
-    jac_to_proj(o, acc);
+    acc_to_proj(o, acc);
     soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
 }
 
@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(kRowsG, 3)
     const int64_t cnt = (int64_t)m * l;
     uint32_t *ob = out + (int64_t)c * kPtWords * cnt;
     const int64_t oi = (int64_t)i * l + j;
-    jacc acc;
-    jac_init(acc);
+    acc_t acc;
+    acc_init(acc);
 #ifdef __CUDA_ARCH__
     if (!first) {
         pt o;
@@ -198,12 +198,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
             o.Y.v[q] = ob[(1 * 8 + q) * cnt + oi];
             o.Z.v[q] = ob[(2 * 8 + q) * cnt + oi];
         }
-        if (!fe_is_zero(o.Z)) {
-            acc.Z = o.Z;
-            acc.ZZ = fe_mul_call(o.Z, o.Z);
-            mul2(acc.X, o.X, o.Z, acc.Y, o.Y, acc.ZZ);
-            acc.inf = 0;
-        }
+        if (!fe_is_zero(o.Z)) acc_from_proj(acc, o);
     }
 #endif
     const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive kk
@@ -219,7 +214,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
             while (kn < kc && rk[(int64_t)kn * m] == 0) kn++;
             fe xn, yn;
             if (kn < kc) load_aff(xn, yn, tb + kn * tstride + (int64_t)rk[(int64_t)kn * m] * kAffWords);
-            jac_add_aff(acc, x2, y2);
+            acc_add_aff(acc, x2, y2);
             if (kn >= kc) break;
             x2 = xn;
             y2 = yn;
@@ -227,7 +222,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
         }
     }
     pt o;
-    jac_to_proj(o, acc);
+    acc_to_proj(o, acc);
     soa_store_hot(ob, cnt, oi, o);
 }
 

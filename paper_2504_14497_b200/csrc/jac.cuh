@@ -183,6 +183,132 @@ __device__ __forceinline__ void jac_dbl(jacc &A) {
 #endif
 }
 
+// ------------------------------------------------------------ XYZZ accumulator
+// x = X/ZZ, y = Y/ZZZ with ZZ^3 = ZZZ^2 (Chudnovsky-style "XYZZ" coordinates).
+// Mixed addition of an affine entry (madd-2008-s): U2 = x2 ZZ1, S2 = y2 ZZZ1,
+// P = U2 - X1, R = S2 - Y1, PP = P^2, PPP = P PP, Q = X1 PP,
+// X3 = R^2 - PPP - 2Q, Y3 = R (Q - X3) - Y1 PPP, ZZ3 = ZZ1 PP, ZZZ3 = ZZZ1 PPP:
+// 8M + 2S in four groups of 2, 2 (squares), 3, 3 independent products, one
+// product fewer than the Jacobian step above (which also has to form Z^3 and
+// Z3 = Z1 H).  Same exceptional cases as jac_add_aff (identity, P = 0), which
+// take the complete RCB16 path on homogeneous images.
+struct xyzz {
+    fe X, Y, ZZ, ZZZ;
+    uint32_t inf;                 // 1 while the accumulator is the identity
+};
+
+__device__ __forceinline__ void xyzz_init(xyzz &A) {
+    fe_zero(A.X);
+    fe_zero(A.Y);
+    fe_zero(A.ZZ);
+    fe_zero(A.ZZZ);
+    A.inf = 1;
+}
+
+// homogeneous (X : Y : Z), Z != 0  ->  XYZZ (X Z, Y Z^2, Z^2, Z^3)
+__device__ __forceinline__ void xyzz_from_proj(xyzz &A, const pt &o) {
+#ifdef __CUDA_ARCH__
+    A.ZZ = fe_mul_call(o.Z, o.Z);
+    mul2(A.X, o.X, o.Z, A.Y, o.Y, A.ZZ);
+    A.ZZZ = fe_mul_call(A.ZZ, o.Z);
+    A.inf = 0;
+#endif
+}
+
+// XYZZ -> homogeneous (X ZZZ : Y ZZ : ZZ ZZZ) (x = X/ZZ, y = Y/ZZZ)
+__device__ __forceinline__ void xyzz_to_proj(pt &o, const xyzz &A) {
+#ifdef __CUDA_ARCH__
+    if (A.inf) {
+        pt_identity(o);
+    } else {
+        mul2(o.X, A.X, A.ZZZ, o.Y, A.Y, A.ZZ);
+        o.Z = fe_mul_call(A.ZZ, A.ZZZ);
+    }
+#endif
+}
+
+static __device__ __noinline__ xyzz xyzz_add_slow(xyzz A, const fe x2, const fe y2) {
+#ifdef __CUDA_ARCH__
+    if (aff_is_inf(x2)) return A;
+    if (A.inf) {
+        A.X = x2;
+        A.Y = y2;
+        fe_one_mont(A.ZZ);
+        A.ZZZ = A.ZZ;
+        A.inf = 0;
+        return A;
+    }
+    pt P, Q, R;
+    xyzz_to_proj(P, A);
+    Q.X = x2;
+    Q.Y = y2;
+    fe_one_mont(Q.Z);
+    pt_add_pair(R, P, Q);                         // complete (RCB16 Alg. 4)
+    if (fe_is_zero(R.Z)) {
+        A.inf = 1;
+        return A;
+    }
+    xyzz_from_proj(A, R);
+#endif
+    return A;
+}
+
+__device__ __forceinline__ void xyzz_add_aff(xyzz &A, const fe &x2, const fe &y2) {
+#ifdef __CUDA_ARCH__
+    if (A.inf | aff_is_inf(x2)) {
+        A = xyzz_add_slow(A, x2, y2);
+        return;
+    }
+    const fe2 us = fe_mul2_hot(x2, A.ZZ, y2, A.ZZZ);   // U2 = x2 ZZ, S2 = y2 ZZZ
+    fe P, R;
+    fe_sub(P, us.x, A.X);
+    if (fe_is_zero(P)) {
+        A = xyzz_add_slow(A, x2, y2);
+        return;
+    }
+    fe_sub(R, us.y, A.Y);
+    const fe2 sq = fe_sqr2_hot(P, R);                  // PP = P^2, R^2
+    const fe &PP = sq.x;
+    const fe3 t = fe_mul3_hot(P, PP, A.X, PP, A.ZZ, PP);   // PPP, Q = X1 PP, ZZ3
+    fe X3, Q2, D;
+    fe_add(Q2, t.y, t.y);
+    fe_sub(X3, sq.y, t.x);
+    fe_sub(X3, X3, Q2);                           // X3 = R^2 - PPP - 2Q
+    fe_sub(D, t.y, X3);
+    const fe3 u = fe_mul3_hot(R, D, A.Y, t.x, A.ZZZ, t.x);  // R (Q - X3), Y1 PPP, ZZZ3
+    fe_sub(A.Y, u.x, u.y);
+    A.X = X3;
+    A.ZZ = t.z;
+    A.ZZZ = u.z;
+#endif
+}
+
+// The accumulate kernels' accumulator (hot.cu): PCMM_ACC_XYZZ=1 (default) XYZZ
+// (8M + 2S per step), 0 the Jacobian step above (9M + 2S).
+#ifndef PCMM_ACC_XYZZ
+#define PCMM_ACC_XYZZ 1
+#endif
+#if PCMM_ACC_XYZZ
+typedef xyzz acc_t;
+__device__ __forceinline__ void acc_init(acc_t &A) { xyzz_init(A); }
+__device__ __forceinline__ void acc_add_aff(acc_t &A, const fe &x, const fe &y) { xyzz_add_aff(A, x, y); }
+__device__ __forceinline__ void acc_to_proj(pt &o, const acc_t &A) { xyzz_to_proj(o, A); }
+__device__ __forceinline__ void acc_from_proj(acc_t &A, const pt &o) { xyzz_from_proj(A, o); }
+#else
+typedef jacc acc_t;
+__device__ __forceinline__ void acc_init(acc_t &A) { jac_init(A); }
+__device__ __forceinline__ void acc_add_aff(acc_t &A, const fe &x, const fe &y) { jac_add_aff(A, x, y); }
+__device__ __forceinline__ void acc_to_proj(pt &o, const acc_t &A) { jac_to_proj(o, A); }
+__device__ __forceinline__ void acc_from_proj(acc_t &A, const pt &o) {
+#ifdef __CUDA_ARCH__
+    A.Z = o.Z;
+    A.ZZ = fe_mul_call(o.Z, o.Z);
+    mul2(A.X, o.X, o.Z, A.Y, o.Y, A.ZZ);
+    A.inf = 0;
+#endif
+}
+#endif
+
 // R = k P for a 256-bit k (little-endian words) and an affine P (x, y) (pinf:
 // the identity): 4-bit fixed windows over precomputed affine multiples 1..15 P
 // (14 mixed additions, one simultaneous inversion), 252 Jacobian doublings and
