@@ -39,9 +39,17 @@ cudaError_t launch_import(const uint8_t *ct, int64_t count, uint32_t *soa, int *
 cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int N, ColPlan *plans, uint8_t *rank,
                         int *status, cudaStream_t s);
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s);
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s,
+                          int skip_fast = 0);   // skip_fast: consecutive columns left to k_tables_fast
 // homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
-cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s);
+// plans != nullptr: entries of consecutive columns (built by k_tables_fast) are skipped
+cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
+                          const ColPlan *plans = nullptr, int n = 0, int l = 0, int S = 0, int N = 0);
+// consecutive columns (s^(1) = {1..n1}): XYZZ prefix sums + fused affine conversion
+// (k_tables_fast); k_tables skips them when tables_fast_on()
+int tables_fast_on();
+cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+                               uint32_t *tables, uint32_t *atables, cudaStream_t s);
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
 // kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
 inline int max_upper(int w) { return w <= 4 ? 8 : 32; }

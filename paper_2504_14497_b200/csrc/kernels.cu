@@ -182,13 +182,20 @@ __device__ __noinline__ void level_n_products_shared(const int16_t *sN, int cnt,
     }
 }
 
+// Column k's tables are built by k_tables_fast (below) when its level-1 set is
+// {1, ..., n1}; k_tables / k_affine then skip it.  (k_affine: plans == nullptr, no skipping)
+__device__ __forceinline__ bool col_consecutive(const ColPlan &pl, int N) {
+    return N >= 2 && pl.n[0] >= 1 && pl.n[1] == 1 && pl.sN[0] == 1;
+}
+
 #ifndef PCMM_TABLES_MINB
 #define PCMM_TABLES_MINB 3
 #endif
 template <bool kSigned>
 __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
                                                    int n, int l, int N, int S, int maxup,
-                                                   uint32_t *__restrict__ tables, uint32_t *__restrict__ scr) {
+                                                   uint32_t *__restrict__ tables, uint32_t *__restrict__ scr,
+                                                   int skip_fast) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -199,6 +206,7 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     const ColPlan &pl = plans[k];
+    if (skip_fast && col_consecutive(pl, N)) return;                 // k_tables_fast
     uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
     uint32_t *sj = scr + j;
     const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;   // in units of l-strided words
@@ -294,28 +302,6 @@ __device__ __forceinline__ void aff_pass1_store(uint32_t *__restrict__ atab, int
     }
 }
 
-__device__ __forceinline__ void aff_pass2_store(const uint32_t *__restrict__ tab, uint32_t *__restrict__ atab,
-                                                int64_t e, const fe &zi) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(tab + e * kPtWords);
-    uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
-    const uint4 x0 = src[0], x1 = src[1], y0 = src[2], y1 = src[3];
-    const fe X = {{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
-    const fe Y = {{y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w}};
-    fe x, y;
-    fe_mul(x, X, zi);
-    fe_mul(y, Y, zi);
-    dst[0] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
-    dst[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
-    dst[2] = make_uint4(y.v[0], y.v[1], y.v[2], y.v[3]);
-    dst[3] = make_uint4(y.v[4], y.v[5], y.v[6], y.v[7]);
-}
-
-__device__ __forceinline__ fe aff_prefix(const uint32_t *__restrict__ atab, int64_t e) {
-    const uint4 *d = reinterpret_cast<const uint4 *>(atab + e * kAffWords);
-    const uint4 p0 = d[2], p1 = d[3];
-    return fe{{p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w}};
-}
-
 __device__ __forceinline__ fe fe_shfl_up(const fe &a, int d) {
     fe r;
 #pragma unroll
@@ -339,22 +325,10 @@ __device__ __forceinline__ fe fe_shfl_down(const fe &a, int d) {
 // SM keep the two passes busy on large tables) or by divsteps (4x shorter latency:
 // small tables, where that one inversion is the kernel's critical path)
 template <bool kFermat>
-__global__ void __launch_bounds__(128) k_affine(const uint32_t *__restrict__ tab, int64_t entries, int batch,
-                                               uint32_t *__restrict__ atab) {
-    __shared__ fe wtot[4], winv[4];
-    const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ fe cta_inverse(const fe &acc, fe *wtot, fe *winv) {
     const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
     fe one;
     fe_one_mont(one);
-    fe acc = one;
-    for (int r = 0; r < batch; r++) {
-        const int64_t e = t + r * T;
-        if (e >= entries) break;
-        const AffIn a0 = aff_load_z(tab, e, entries);
-        aff_pass1_store(atab, e, entries, a0, acc);
-        if (a0.ok) fe_mul(acc, acc, a0.z);
-    }
     // warp-inclusive prefix (Q) and suffix (S) products of the lane products
     fe Q = acc, S = acc;
 #pragma unroll
@@ -391,15 +365,260 @@ __global__ void __launch_bounds__(128) k_affine(const uint32_t *__restrict__ tab
     fe inv;
     fe_mul(inv, winv[warp], qprev);
     fe_mul(inv, inv, snext);                       // 1 / acc (this lane's product)
-    for (int r = batch - 1; r >= 0; r--) {
+    return inv;
+}
+
+// Entry kinds for k_affine: homogeneous (X : Y : Z) from k_tables, or, in a
+// consecutive column (k_tables_fast), slots 2..n1 hold XYZZ (X, Y, ZZ in the
+// projective slot, ZZZ in the x half of the affine slot: 1/ZZZ from the batch,
+// 1/Z = ZZ/ZZZ, x = X/Z^2, y = Y/ZZZ) and the other slots are already final.
+enum { kAffSkip = 0, kAffProj = 1, kAffXyzz = 2 };
+#ifndef PCMM_TFAST_PROJ
+#define PCMM_TFAST_PROJ 0       // 1: k_tables_fast stores homogeneous (X ZZZ : Y ZZ : ZZ ZZZ) entries instead
+#endif
+
+__device__ __forceinline__ AffIn aff_load_zzz(const uint32_t *__restrict__ atab, int64_t e) {
+    AffIn a;
+    const uint4 *src = reinterpret_cast<const uint4 *>(atab + e * kAffWords);
+    const uint4 z0 = src[0], z1 = src[1];
+    a.z = fe{{z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w}};
+    a.ok = (z0.x | z0.y | z0.z | z0.w | z1.x | z1.y | z1.z | z1.w) != 0;
+    return a;
+}
+
+// One table entry's inputs for the second pass, loaded one iteration ahead
+struct AffEnt {
+    fe X, Y, Z, pre;      // Z: homogeneous Z, or ZZ of an XYZZ entry; pre = prefix product
+    fe zz3;               // ZZZ of an XYZZ entry
+    int kind;
+    bool ok;
+};
+
+__device__ __forceinline__ void aff_fetch(AffEnt &a, const uint32_t *__restrict__ tab,
+                                          const uint32_t *__restrict__ atab, int64_t e, int kind) {
+    a.kind = kind;
+    a.ok = false;
+    if (kind == kAffSkip) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(tab + e * kPtWords);
+    const uint4 x0 = src[0], x1 = src[1], y0 = src[2], y1 = src[3], z0 = src[4], z1 = src[5];
+    a.X = fe{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
+    a.Y = fe{{y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w}};
+    a.Z = fe{{z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w}};
+    const uint4 *d = reinterpret_cast<const uint4 *>(atab + e * kAffWords);
+    const uint4 q0 = d[0], q1 = d[1], p0 = d[2], p1 = d[3];
+    a.pre = fe{{p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w}};
+    if (kind == kAffXyzz) {
+        a.zz3 = fe{{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w}};
+        a.ok = !fe_is_zero(a.zz3);
+    } else {
+        a.ok = !fe_is_zero(a.Z);
+    }
+}
+
+#ifndef PCMM_AFFINE_MINB
+#define PCMM_AFFINE_MINB 4
+#endif
+template <bool kFermat>
+__global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t *__restrict__ tab, int64_t entries,
+                                                                  int batch, uint32_t *__restrict__ atab,
+                                                                  const ColPlan *__restrict__ plans, int n, int l,
+                                                                  int S, int N) {
+    __shared__ fe wtot[4], winv[4];
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // entry e = ((c n + k) l + j) S + slot; plans != nullptr only on the byte path
+    // (entries = 2 n l S < 2^32, S a power of two): 32-bit index arithmetic
+    const uint32_t sl = (uint32_t)S * (uint32_t)l;
+    auto kind = [&](int64_t e) -> int {
+        if (e >= entries) return kAffSkip;
+        if (plans == nullptr) return kAffProj;
+        const uint32_t e32 = (uint32_t)e;
+        const ColPlan &pl = plans[(e32 / sl) % (uint32_t)n];
+        if (!col_consecutive(pl, N)) return kAffProj;
+        const int slot = (int)(e32 & (uint32_t)(S - 1));
+        return (slot >= 2 && slot <= pl.n[0]) ? (PCMM_TFAST_PROJ ? kAffProj : kAffXyzz) : kAffSkip;
+    };
+    fe one;
+    fe_one_mont(one);
+    fe acc = one;
+    int any = 0;
+    for (int r = 0; r < batch; r++) {
         const int64_t e = t + r * T;
-        if (e >= entries) continue;
-        const AffIn a0 = aff_load_z(tab, e, entries);
-        if (!a0.ok) continue;
-        fe zi;
-        fe_mul(zi, inv, aff_prefix(atab, e));      // 1 / Z_e
-        fe_mul(inv, inv, a0.z);                    // 1 / (product of this lane's Z before e)
-        aff_pass2_store(tab, atab, e, zi);
+        if (e >= entries) break;
+        const int kd = kind(e);
+        if (kd == kAffSkip) continue;
+        const AffIn a0 = kd == kAffProj ? aff_load_z(tab, e, entries) : aff_load_zzz(atab, e);
+        if (kd == kAffProj || !a0.ok) {
+            aff_pass1_store(atab, e, entries, a0, acc);
+        } else {
+            uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
+            dst[2] = make_uint4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
+            dst[3] = make_uint4(acc.v[4], acc.v[5], acc.v[6], acc.v[7]);
+        }
+        if (a0.ok) {
+            fe_mul(acc, acc, a0.z);
+            any = 1;
+        }
+    }
+    if (!__syncthreads_or(any)) return;                                // nothing to invert in this CTA
+    fe inv = cta_inverse<kFermat>(acc, wtot, winv);
+    AffEnt cur;
+    int r = batch - 1;
+    aff_fetch(cur, tab, atab, t + r * T, kind(t + r * T));
+    for (; r >= 0; r--) {
+        const int64_t e = t + r * T;
+        AffEnt nxt;
+        nxt.kind = kAffSkip;
+        nxt.ok = false;
+        if (r > 0) aff_fetch(nxt, tab, atab, e - T, kind(e - T));   // next entry's loads in flight
+        if (cur.ok) {
+            fe ui, x, y;
+            fe_mul(ui, inv, cur.pre);              // 1 / Z (homogeneous) or 1 / ZZZ (XYZZ)
+            if (cur.kind == kAffProj) {
+                fe_mul(inv, inv, cur.Z);
+                fe_mul(x, cur.X, ui);
+                fe_mul(y, cur.Y, ui);
+            } else {
+                fe zi, zi2;
+                fe_mul(inv, inv, cur.zz3);
+                fe_mul(zi, ui, cur.Z);             // 1 / Z = ZZ / ZZZ
+                fe_sqr(zi2, zi);
+                fe_mul(x, cur.X, zi2);
+                fe_mul(y, cur.Y, ui);
+            }
+            uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
+            dst[0] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+            dst[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+            dst[2] = make_uint4(y.v[0], y.v[1], y.v[2], y.v[3]);
+            dst[3] = make_uint4(y.v[4], y.v[5], y.v[6], y.v[7]);
+        }
+        cur = nxt;
+    }
+}
+
+// ------------------------------------------------------------ a2 + a3 for consecutive columns
+// When s^(1)_k = {1, ..., n1} (every unsigned w <= 4 column of a dense random A),
+// Alg. 2 gives s^(2) = ... = s^(N) = {1}: no ECSM (x1 is free, Alg. 3 line 5) and
+// the level-1 reconstruction is the prefix sum T[u] = T[u-1] + P with the
+// ciphertext component P itself as every addend (Alg. 2 lines 14-23).  P is
+// affine (k_import: Z = 1), so each step is an XYZZ mixed addition (8M + 2S,
+// jac.cuh) instead of a complete projective addition (12M + 2m_b), and T[2] = 2P
+// an affine-input doubling (4M + 3S).  The XYZZ entries go to k_affine (6M + 1S
+// per entry there, against 5M for a homogeneous one).  Other columns: k_tables.
+__device__ __forceinline__ void xyzz_dbl_aff(xyzz &A, const fe &x, const fe &y) {
+    fe U, V, W, Sv, M, x2, t, X3, D;
+    fe_add(U, y, y);                               // U = 2y
+    fe_sqr(V, U);                                  // V = U^2
+    fe_mul(W, U, V);                               // W = U V
+    fe_mul(Sv, x, V);                              // S = x V
+    fe_sqr(x2, x);
+    fe one;
+    fe_one_mont(one);
+    fe_sub(t, x2, one);
+    fe_add(M, t, t);
+    fe_add(M, M, t);                               // M = 3 (x^2 - 1) = 3 x^2 + a, a = -3
+    fe_sqr(X3, M);
+    fe_sub(X3, X3, Sv);
+    fe_sub(X3, X3, Sv);                            // X3 = M^2 - 2S
+    fe_sub(D, Sv, X3);
+    fe_mul(D, M, D);
+    fe_mul(t, W, y);
+    fe_sub(A.Y, D, t);                             // Y3 = M (S - X3) - W y
+    A.X = X3;
+    A.ZZ = V;
+    A.ZZZ = W;
+    A.inf = 0;
+}
+
+__device__ __forceinline__ void st_fe2(uint32_t *d, const fe &a, const fe &b) {
+    uint4 *q = reinterpret_cast<uint4 *>(d);
+    q[0] = make_uint4(a.v[0], a.v[1], a.v[2], a.v[3]);
+    q[1] = make_uint4(a.v[4], a.v[5], a.v[6], a.v[7]);
+    q[2] = make_uint4(b.v[0], b.v[1], b.v[2], b.v[3]);
+    q[3] = make_uint4(b.v[4], b.v[5], b.v[6], b.v[7]);
+}
+
+__device__ __forceinline__ void ld_fe2(fe &a, fe &b, const uint32_t *d) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(d);
+    const uint4 a0 = q[0], a1 = q[1], b0 = q[2], b1 = q[3];
+    a = fe{{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}};
+    b = fe{{b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w}};
+}
+
+__device__ __forceinline__ void st_aff_inf(uint32_t *d) {
+    uint4 *q = reinterpret_cast<uint4 *>(d);
+    const uint4 ones = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    q[0] = ones;
+    q[1] = ones;
+    q[2] = make_uint4(0, 0, 0, 0);
+    q[3] = make_uint4(0, 0, 0, 0);
+}
+
+#ifndef PCMM_TFAST_MINB
+#define PCMM_TFAST_MINB 3
+#endif
+__global__ void __launch_bounds__(128, PCMM_TFAST_MINB)
+    k_tables_fast(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans, int n, int l, int N, int S,
+                  uint32_t *__restrict__ tables, uint32_t *__restrict__ atab) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = 2LL * n * l;
+    if (t >= total) return;
+    const int j = (int)(t % l);
+    const int k = (int)((t / l) % n);
+    const int c = (int)(t / ((int64_t)l * n));
+    const ColPlan &pl = plans[k];
+    if (!col_consecutive(pl, N)) return;                              // k_tables + k_affine
+    const int64_t cnt = (int64_t)n * l;
+    pt P;
+    soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
+    const int64_t tb = ((int64_t)c * n + k) * l + j;
+    uint32_t *blk = tables + tb * (int64_t)(kPtWords * S);
+    uint32_t *ablk = atab + tb * (int64_t)(kAffWords * S);
+    const int n1 = pl.n[0];
+    fe zero;
+    fe_zero(zero);
+    st_aff_inf(ablk);                                                 // slot 0 = the identity
+    for (int u = n1 + 1; u < S; u++) st_aff_inf(ablk + u * kAffWords);
+    if (pt_is_identity(P)) {                                          // every multiple is the identity
+        st_aff_inf(ablk + kAffWords);
+        for (int u = 2; u <= n1; u++) {
+#if PCMM_TFAST_PROJ
+            pt id;
+            pt_identity(id);
+            table_store(blk, u, id);
+#else
+            st_fe2(ablk + u * kAffWords, zero, zero);                 // ZZZ = 0: k_affine -> identity
+#endif
+        }
+        return;
+    }
+    st_fe2(ablk + kAffWords, P.X, P.Y);                               // T[1] = P (Z = 1)
+    xyzz run;
+    for (int u = 2; u <= n1; u++) {
+        if (u == 2) xyzz_dbl_aff(run, P.X, P.Y);
+        else xyzz_add_aff(run, P.X, P.Y);
+        if (run.inf) {                                                // only off the curve
+#if PCMM_TFAST_PROJ
+            pt id;
+            pt_identity(id);
+            table_store(blk, u, id);
+#else
+            st_fe2(ablk + u * kAffWords, zero, zero);
+#endif
+            continue;
+        }
+        uint32_t *e = blk + u * kPtWords;
+#if PCMM_TFAST_PROJ
+        pt h;
+        xyzz_to_proj(h, run);
+        table_store(blk, u, h);
+#else
+        st_fe2(e, run.X, run.Y);
+        uint4 *z = reinterpret_cast<uint4 *>(e + 16);
+        z[0] = make_uint4(run.ZZ.v[0], run.ZZ.v[1], run.ZZ.v[2], run.ZZ.v[3]);
+        z[1] = make_uint4(run.ZZ.v[4], run.ZZ.v[5], run.ZZ.v[6], run.ZZ.v[7]);
+        st_fe2(ablk + u * kAffWords, run.ZZZ, zero);                  // ZZZ parked in the affine slot
+#endif
     }
 }
 
@@ -695,7 +914,8 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s) {
+cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
+                          const ColPlan *plans, int n, int l, int S, int N) {
     if (entries <= 0) return cudaSuccess;
     // up to 32 entries per lane (one inversion per 4096 entries), fewer when that
     // would leave fewer than ~4 warps per SM (256^3: batch 32 0.48 ms, 16 0.55, 8 0.76)
@@ -708,17 +928,43 @@ cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *ata
     const int batch = batch_env > 0 ? batch_env : (int)std::min<int64_t>(32, std::max<int64_t>(1, entries / want));
     const int64_t threads = (entries + batch - 1) / batch;
     // 256^3 (2.1 M entries): Fermat 0.29 ms vs divsteps 0.36; 64^3 (131 K): 0.113 vs 0.084
-    if (entries >= (1 << 20)) k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables);
-    else k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables);
+    static int inv_env = -2;
+    if (inv_env == -2) {
+        const char *e = getenv("PCMM_AFFINE_FERMAT");         // measurement override: 1 Fermat, 0 divsteps
+        inv_env = e ? atoi(e) : -1;
+    }
+    if (inv_env == 1 || (inv_env < 0 && entries >= (1 << 20)))
+        k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
+    else
+        k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
     return cudaGetLastError();
 }
 
+static int tables_fast_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PCMM_TABLES_FAST");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s, int fast) {
     if (is_signed)
-        k_tables<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+        k_tables<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch,
+                                                                    fast);
     else
-        k_tables<false><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+        k_tables<false><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables,
+                                                                     scratch, fast);
+    return cudaGetLastError();
+}
+
+int tables_fast_on() { return tables_fast_enabled(); }
+
+cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+                               uint32_t *tables, uint32_t *atables, cudaStream_t s) {
+    k_tables_fast<<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, tables, atables);
     return cudaGetLastError();
 }
 

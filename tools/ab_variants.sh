@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B: run quick parity + c256 bench for each prebuilt libpcmm variant in variants/
 cp paper_2504_14497_b200/libpcmm.so /tmp/lib_orig.so
-for v in variants/*.so; do
+for v in ${VARDIR:-variants}/*.so; do
   cp $v paper_2504_14497_b200/libpcmm.so
   touch paper_2504_14497_b200/libpcmm.so
   r=$(python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -W ignore -k "c64 or field or ragged" 2>&1 | tail -1)
