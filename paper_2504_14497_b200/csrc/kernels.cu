@@ -386,6 +386,15 @@ __device__ __forceinline__ AffIn aff_load_zzz(const uint32_t *__restrict__ atab,
     return a;
 }
 
+__device__ __forceinline__ void st_aff_inf(uint32_t *d) {
+    uint4 *q = reinterpret_cast<uint4 *>(d);
+    const uint4 ones = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    q[0] = ones;
+    q[1] = ones;
+    q[2] = make_uint4(0, 0, 0, 0);
+    q[3] = make_uint4(0, 0, 0, 0);
+}
+
 // One table entry's inputs for the second pass, loaded one iteration ahead
 struct AffEnt {
     fe X, Y, Z, pre;      // Z: homogeneous Z, or ZZ of an XYZZ entry; pre = prefix product
@@ -448,9 +457,9 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
         const int kd = kind(e);
         if (kd == kAffSkip) continue;
         const AffIn a0 = kd == kAffProj ? aff_load_z(tab, e, entries) : aff_load_zzz(atab, e);
-        if (kd == kAffProj || !a0.ok) {
+        if (kd == kAffProj) {
             aff_pass1_store(atab, e, entries, a0, acc);
-        } else {
+        } else if (a0.ok) {                                            // ZZZ = 0 stays for pass 2
             uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
             dst[2] = make_uint4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
             dst[3] = make_uint4(acc.v[4], acc.v[5], acc.v[6], acc.v[7]);
@@ -491,6 +500,8 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
             dst[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
             dst[2] = make_uint4(y.v[0], y.v[1], y.v[2], y.v[3]);
             dst[3] = make_uint4(y.v[4], y.v[5], y.v[6], y.v[7]);
+        } else if (cur.kind == kAffXyzz) {
+            st_aff_inf(atab + e * kAffWords);      // ZZZ = 0: the identity
         }
         cur = nxt;
     }
@@ -545,14 +556,6 @@ __device__ __forceinline__ void ld_fe2(fe &a, fe &b, const uint32_t *d) {
     b = fe{{b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w}};
 }
 
-__device__ __forceinline__ void st_aff_inf(uint32_t *d) {
-    uint4 *q = reinterpret_cast<uint4 *>(d);
-    const uint4 ones = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-    q[0] = ones;
-    q[1] = ones;
-    q[2] = make_uint4(0, 0, 0, 0);
-    q[3] = make_uint4(0, 0, 0, 0);
-}
 
 #ifndef PCMM_TFAST_MINB
 #define PCMM_TFAST_MINB 3

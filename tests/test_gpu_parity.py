@@ -219,6 +219,31 @@ def test_degenerate_matrices():
     assert (_gpu_pcmm(I.A, ct2, 8, 4, False, P.CUSSEN) == exp).all()
 
 
+@pytest.mark.parametrize("w", [2, 4])
+def test_consecutive_column_tables_mixed(w):
+    # A launch large enough for k_tables_fast (2 n l >= 65536): columns whose level-1
+    # set is {1..n1} (built by XYZZ prefix sums, converted by k_affine's XYZZ branch)
+    # next to columns that are not (k_tables + homogeneous k_affine), an all-zero
+    # column, and identity ciphertexts in a consecutive column.
+    m, n, l = 8, 256, 128
+    cfg = synth.Config("mixed", m, n, l, w, False, 0, 255, 77 + w)
+    I = synth.make_instance(cfg)
+    A = I.A.copy()
+    top = (1 << w) - 1
+    A[:, 0] = [(i % top) + 1 for i in range(m)]        # consecutive, n1 = min(m, top)
+    A[:, 1] = 2                                          # {2}: not consecutive
+    A[:, 2] = 0                                          # empty column
+    A[:, 3] = [1, 3] * (m // 2)                          # {1, 3}: not consecutive
+    A[:, 4] = [1, 2] * (m // 2)                          # consecutive, n1 = 2
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct[0, 5] = 0                                         # (inf, inf) in consecutive column k = 0
+    ct[4, :7, 64:] = 0                                   # C2 = inf in k = 4
+    ct = np.ascontiguousarray(ct.reshape(n * l, 128))
+    exp, _ = oracle.pcmm(oracle.CUSSEN, A, ct, l, w)
+    assert (_gpu_pcmm(A, ct, l, w, False, P.CUSSEN) == exp).all()
+
+
 @pytest.mark.parametrize("w", [4, 6])
 def test_accumulator_exceptional_cases(w):
     # Equal ciphertexts in rows k = 0..3 make the accumulated sum equal to +-(the next
