@@ -69,7 +69,7 @@ def ncu_summary(rep, tag):
 
 launches()
 t_acc = ncu_summary(os.path.join(OUT, "prof_accum.ncu-rep"), "k_accum")
-t_tab = ncu_summary(os.path.join(OUT, "prof_tables.ncu-rep"), "k_tables")
+t_tab = ncu_summary(os.path.join(OUT, "prof_tables.ncu-rep"), "k_tables_fast")
 t_aff = ncu_summary(os.path.join(OUT, "prof_affine.ncu-rep"), "k_affine")
 tj = os.path.join(PROF, "traffic.json")
 data = json.load(open(tj)) if os.path.exists(tj) else {}
