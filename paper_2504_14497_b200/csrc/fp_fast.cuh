@@ -524,6 +524,27 @@ __device__ PCMM_HOTCALL fe2 fe_sqr2_hot(const fe a, const fe b) {
     return r;
 }
 
+// (c^2, a0 b0, a1 b1, a2 b2) and four products: the software-pipelined XYZZ step
+__device__ PCMM_HOTCALL fe4 fe_sqr_mul3_hot(const fe c, const fe a0, const fe b0, const fe a1, const fe b1,
+                                            const fe a2, const fe b2) {
+    fe4 r;
+    fe_sqr_fast(r.x, c);
+    fe_mul_fast(r.y, a0, b0);
+    fe_mul_fast(r.z, a1, b1);
+    fe_mul_fast(r.w, a2, b2);
+    return r;
+}
+
+__device__ PCMM_HOTCALL fe4 fe_mul4_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
+                                        const fe b2, const fe a3, const fe b3) {
+    fe4 r;
+    fe_mul_fast(r.x, a0, b0);
+    fe_mul_fast(r.y, a1, b1);
+    fe_mul_fast(r.z, a2, b2);
+    fe_mul_fast(r.w, a3, b3);
+    return r;
+}
+
 __device__ PCMM_HOTCALL fe3 fe_mul3_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
                                         const fe b2) {
     fe3 r;

@@ -28,8 +28,22 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #ifndef PCMM_ACCUM_CHUNK_SLOTS
 #define PCMM_ACCUM_CHUNK_SLOTS 512  // table slots staged per chunk: k-chunk = this / 2^w (32 at w = 4)
 #endif
+#ifndef PCMM_ACC_PIPE
+#define PCMM_ACC_PIPE 1         // software-pipelined XYZZ step (jac.cuh xyzz_add_aff_pipe); needs PCMM_ACC_XYZZ
+#endif
+#if !PCMM_ACC_XYZZ
+#undef PCMM_ACC_PIPE
+#define PCMM_ACC_PIPE 0
+#endif
 #ifndef PCMM_ACCUM_MINB
-#define PCMM_ACCUM_MINB 4       // resident CTAs per SM the register allocation targets (4: 128 regs, 5: 96)
+// resident CTAs per SM the register allocation targets (3: 168 regs, 4: 128, 5: 96).  The pipelined
+// step's 4-product groups spill at 128 registers (256^3 accumulate +6 %); at 3 CTAs per SM it is 1.7 %
+// faster than the 4-group step at 4 CTAs per SM (which is 2 % slower at 3)
+#if PCMM_ACC_PIPE
+#define PCMM_ACCUM_MINB 3
+#else
+#define PCMM_ACCUM_MINB 4
+#endif
 #endif
 
 template <int S>
@@ -95,6 +109,37 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
         // each lane walks its own nonzero entries (zeros are the identity, skipped)
         int kk = 0;
         while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
+#if PCMM_ACC_PIPE
+        if (kk < kc) {
+            fe x2, y2, U2;
+            bool have_u2 = false;
+            {
+                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    x2.v[q] = T[q];
+                    y2.v[q] = T[8 + q];
+                }
+            }
+            while (true) {
+                int kn = kk + 1;
+                while (kn < kc && rsm[kn * ROWS + tid] == 0) kn++;
+                const bool more = kn < kc;
+                const uint32_t *T = tsm + (more ? kn * TWS + rsm[kn * ROWS + tid] * EW : kk * TWS + rsm[kk * ROWS + tid] * EW);
+                fe xn, yn;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    xn.v[q] = T[q];
+                    yn.v[q] = T[8 + q];
+                }
+                xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);
+                if (!more) break;
+                x2 = xn;
+                y2 = yn;
+                kk = kn;
+            }
+        }
+#else
         while (kk < kc) {
             const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
             fe x2, y2;
@@ -107,6 +152,7 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
             kk++;
             while (kk < kc && rsm[kk * ROWS + tid] == 0) kk++;
         }
+#endif
     }
     if (i < m) {
         const int64_t cnt = (int64_t)m * l;

@@ -283,6 +283,48 @@ __device__ __forceinline__ void xyzz_add_aff(xyzz &A, const fe &x2, const fe &y2
 #endif
 }
 
+// Software-pipelined form for the shared-memory accumulate loop: the next entry's
+// U2' = x2' ZZ3 needs only ZZ3, so it joins the last product group of this step,
+// and S2 = y2 ZZZ joins P^2:  {S2, PP} | {R^2, PPP, Q, ZZ3} | {R (Q - X3), Y1 PPP,
+// ZZZ3, U2'}: three dependent groups of 2, 4, 4 products per step instead of four
+// of 2, 2, 3, 3, the same 8M + 2S (U2' is this step's share of the next one).
+// have_u2: U2 holds x2 ZZ for the current accumulator (false after the general
+// path or at the start of a chunk: then it is computed here).  xn: the next
+// entry's x (any residue when there is none: the extra product is discarded).
+__device__ __forceinline__ void xyzz_add_aff_pipe(xyzz &A, const fe &x2, const fe &y2, fe &U2, bool &have_u2,
+                                                  const fe &xn) {
+#ifdef __CUDA_ARCH__
+    if (A.inf | aff_is_inf(x2)) {
+        A = xyzz_add_slow(A, x2, y2);
+        have_u2 = false;
+        return;
+    }
+    if (!have_u2) U2 = fe_mul_call(x2, A.ZZ);
+    fe P, R;
+    fe_sub(P, U2, A.X);
+    if (fe_is_zero(P)) {
+        A = xyzz_add_slow(A, x2, y2);
+        have_u2 = false;
+        return;
+    }
+    const fe2 sp = fe_mulsqr_hot(y2, A.ZZZ, P);              // S2 = y2 ZZZ, PP = P^2
+    fe_sub(R, sp.x, A.Y);
+    const fe4 t = fe_sqr_mul3_hot(R, P, sp.y, A.X, sp.y, A.ZZ, sp.y);   // R^2, PPP, Q = X1 PP, ZZ3
+    fe X3, Q2, D;
+    fe_add(Q2, t.z, t.z);
+    fe_sub(X3, t.x, t.y);
+    fe_sub(X3, X3, Q2);                                     // X3 = R^2 - PPP - 2Q
+    fe_sub(D, t.z, X3);
+    const fe4 u = fe_mul4_hot(R, D, A.Y, t.y, A.ZZZ, t.y, xn, t.w);   // R (Q - X3), Y1 PPP, ZZZ3, U2'
+    fe_sub(A.Y, u.x, u.y);
+    A.X = X3;
+    A.ZZ = t.w;
+    A.ZZZ = u.z;
+    U2 = u.w;
+    have_u2 = true;
+#endif
+}
+
 // The accumulate kernels' accumulator (hot.cu): PCMM_ACC_XYZZ=1 (default) XYZZ
 // (8M + 2S per step), 0 the Jacobian step above (9M + 2S).
 #ifndef PCMM_ACC_XYZZ
