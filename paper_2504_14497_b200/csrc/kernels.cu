@@ -942,7 +942,9 @@ cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *ata
         const char *e = getenv("PCMM_AFFINE_FERMAT");         // measurement override: 1 Fermat, 0 divsteps
         inv_env = e ? atoi(e) : -1;
     }
-    if (inv_env == 1 || (inv_env < 0 && entries >= (1 << 20)))
+    // with the one-wave batch and 128 registers (PCMM_AFFINE_MINB) divsteps win everywhere:
+    // 256^3 0.309 vs 0.324 ms, 512^3 0.299 vs 0.314, ML 0.246 vs 0.261, 64^3 0.091 vs 0.107
+    if (inv_env == 1)
         k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
     else
         k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
