@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
 // ------------------------------------------------------------ a4 (wide path, NEXT-1): one k-chunk
 // As k_accum_g for the chunk k0 .. k0+kc-1 of the wide path (wide.cu): uint16
 // rank, tables [c][kk][j][slot][16].  The accumulator starts from the running
-// output (homogeneous (X : Y : Z) -> Jacobian (X Z, Y Z^2, Z)) unless this is
+// output (homogeneous (X : Y : Z) -> XYZZ (X Z, Y Z^2, Z^2, Z^3)) unless this is
 // the first chunk, and the chunk's sum is written back to it.
 __global__ void __launch_bounds__(kRowsG, 3)
     k_accum_gw(const uint32_t *__restrict__ tables, const uint16_t *__restrict__ rank, int m, int l, int S, int k0,

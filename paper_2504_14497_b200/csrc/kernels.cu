@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
 }
 
 // ------------------------------------------------------------ a3': tables -> affine
-// The accumulate loop adds table entries with the Jacobian + affine mixed
+// The accumulate loop adds table entries with the XYZZ + affine mixed
 // addition (hot.cu), so the tables are converted once to affine (x, y) =
 // (X/Z, Y/Z) with Montgomery's simultaneous inversion: each lane takes `batch`
 // entries (stride = grid size, so a warp reads consecutive entries), one fe_inv
