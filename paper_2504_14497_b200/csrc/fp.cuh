@@ -410,8 +410,11 @@ PCMM_HD void fe_inv_plain_divsteps(fe &r, const fe &x) {
         e.v[i] = i == 0 ? 1 : 0;
     }
     int32_t zeta = -1;
+    // zeta = -(delta + 1/2) with delta starting at 1/2: the "half-delta" divstep, for which
+    // 590 divsteps suffice for 256-bit inputs (Bernstein-Yang's bound, as used by
+    // libsecp256k1's constant-time modinv): 20 batches of 30
 #pragma unroll 1
-    for (int it = 0; it < 25; it++) {
+    for (int it = 0; it < 20; it++) {
         int32_t M[4];
         zeta = divsteps30(zeta, (uint32_t)f.v[0] | ((uint32_t)f.v[1] << 30), (uint32_t)g.v[0] | ((uint32_t)g.v[1] << 30),
                           M);
@@ -428,11 +431,111 @@ PCMM_HD void fe_inv_plain_divsteps(fe &r, const fe &x) {
     s30_to_words(r, d);
 }
 
+// Variable-time divsteps (original delta, eta = -delta starting at -1): runs of even g
+// are shifted out at once (count trailing zeros) and an odd g has its low
+// min(eta + 1, remaining, 8) bits cancelled by adding w f, w = -g / f mod 2^8 (f^-1 by
+// two Newton steps) -- the same 30-divstep transition matrix as divsteps30 in far
+// fewer loop trips.  Side channels are out of scope (DESIGN R11).
+PCMM_HD int ctz32_hd(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __ffs((int)x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+
+PCMM_HD int32_t divsteps30_var(int32_t eta, uint32_t f, uint32_t g, int32_t M[4]) {
+    uint32_t u = 1, v = 0, q = 0, r = 1;
+    int i = 30;
+    for (;;) {
+        const int zeros = ctz32_hd(g | (0xffffffffu << i));
+        g >>= zeros;
+        u <<= zeros;
+        v <<= zeros;
+        eta -= zeros;
+        i -= zeros;
+        if (i == 0) break;
+        if (eta < 0) {                                          // (f, g) <- (g, -f)
+            uint32_t t;
+            eta = -eta;
+            t = f; f = g; g = 0u - t;
+            t = u; u = q; q = 0u - t;
+            t = v; v = r; r = 0u - t;
+        }
+        const int limit = (eta + 1) > i ? i : (eta + 1);
+        const uint32_t m = (0xffffffffu >> (32 - limit)) & 255u;
+        uint32_t fi = f;                                         // f odd: f f = 1 mod 8
+        fi *= 2u - f * fi;                                       // f^-1 mod 2^6
+        fi *= 2u - f * fi;                                       // f^-1 mod 2^12
+        const uint32_t w = (0u - g * fi) & m;
+        g += f * w;
+        q += u * w;
+        r += v * w;
+    }
+    M[0] = (int32_t)u;
+    M[1] = (int32_t)v;
+    M[2] = (int32_t)q;
+    M[3] = (int32_t)r;
+    return eta;
+}
+
+PCMM_HD bool s30_is_zero(const s30 &a) {
+    int32_t o = 0;
+    for (int i = 0; i < 9; i++) o |= a.v[i];
+    return o == 0;
+}
+
+// plain x^-1 mod p by variable-time divsteps, stopping as soon as g = 0 (<= 25
+// batches: the original divstep needs <= 741 steps for 256-bit inputs)
+PCMM_HD void fe_inv_plain_divsteps_var(fe &r, const fe &x) {
+    fe pw;
+    for (int i = 0; i < 8; i++) pw.v[i] = p_limb(i);
+    s30 P, f, g, d, e;
+    s30_from_words(P, pw);
+    f = P;
+    s30_from_words(g, x);
+    for (int i = 0; i < 9; i++) {
+        d.v[i] = 0;
+        e.v[i] = i == 0 ? 1 : 0;
+    }
+    int32_t eta = -1;
+#pragma unroll 1
+    for (int it = 0; it < 26 && !s30_is_zero(g); it++) {
+        int32_t M[4];
+        eta = divsteps30_var(eta, (uint32_t)f.v[0] | ((uint32_t)f.v[1] << 30), (uint32_t)g.v[0] | ((uint32_t)g.v[1] << 30),
+                             M);
+        s30_apply_de(d, e, M, P);
+        s30_apply_fg(f, g, M);
+    }
+    if (s30_neg(f)) {
+        s30 z;
+        for (int i = 0; i < 9; i++) z.v[i] = 0;
+        s30_addmul(d, z, d, -1);
+        if (s30_neg(d)) s30_addmul(d, d, P, 1);
+    }
+    s30_to_words(r, d);
+}
+
+PCMM_HD_NOINLINE void fe_inv_var(fe &r, const fe &a) {
+    fe inv, r2;
+    fe_inv_plain_divsteps_var(inv, a);
+    fe_r2(r2);
+    fe_mul(inv, inv, r2);
+    fe_mul(r, inv, r2);
+}
+
 // r = a^-1 in Montgomery form: plain inverse of the Montgomery residue a R, times R^3
 // (two Montgomery products by R^2 mod p): (a R)^-1 R^2 = a^-1 R.  0 -> 0.
+#ifndef PCMM_INV_VAR
+#define PCMM_INV_VAR 1          // 1: fe_inv runs the variable-time divsteps (256^3: k_normalize 0.091 -> 0.082 ms, k_affine 0.302 -> 0.289; tiny 0.200 -> 0.188 ms); 0: constant-time
+#endif
 PCMM_HD_NOINLINE void fe_inv(fe &r, const fe &a) {
     fe inv, r2;
+#if PCMM_INV_VAR
+    fe_inv_plain_divsteps_var(inv, a);
+#else
     fe_inv_plain_divsteps(inv, a);
+#endif
     fe_r2(r2);
     fe_mul(inv, inv, r2);
     fe_mul(r, inv, r2);

@@ -25,6 +25,7 @@ int hfp_op(int op, const uint8_t *a_be, const uint8_t *b_be, uint8_t *out_be) {
         case 3: fe_inv(r, a); break;
         case 4: fe_neg(r, a); break;
         case 5: fe_inv_fermat(r, a); break;
+        case 6: fe_inv_var(r, a); break;
         default: return -1;
     }
     fe_from_mont(r, r);

@@ -43,6 +43,8 @@ rng = random.Random(1234)
 # ------------------------------------------------------------------ field / points
 def test_field_ops_bit_exact():
     vals = [0, 1, 2, ecref.P - 1, ecref.P - 2, 2**224, 2**96 - 1] + [rng.randrange(ecref.P) for _ in range(4000)]
+    # structured inputs for the variable-time inversion (long runs of zero / one bits)
+    vals += [2**k for k in range(256)] + [(2**k - 1) % ecref.P for k in range(1, 257)] + [ecref.P - 2**k for k in range(0, 224, 5)]
     a = vals
     b = [rng.choice(vals) for _ in vals]
     A = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in a), dtype=np.uint8).reshape(-1, 32))

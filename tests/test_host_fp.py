@@ -65,8 +65,28 @@ def test_field_ops_vs_python_ints():
         if a:
             assert get(3) == pow(a, -1, P)                 # divsteps (Bernstein-Yang)
             assert get(5) == pow(a, -1, P)                 # Fermat chain
+            assert get(6) == pow(a, -1, P)                 # variable-time divsteps
         else:
-            assert get(3) == 0 and get(5) == 0
+            assert get(3) == 0 and get(5) == 0 and get(6) == 0
+
+
+def test_inversions_many_inputs():
+    # divsteps (20 batches of 30 half-delta steps), variable-time divsteps and Fermat agree with
+    # pow(a, -1, p) on structured inputs (runs of zero / one bits, tiny and near-p values) and
+    # thousands of random ones
+    P = ecref.P
+    vals = [1, 2, 3, P - 1, P - 2, 2**255 % P, P >> 1, (P + 1) >> 1]
+    vals += [2**k for k in range(0, 256)] + [(2**k - 1) % P for k in range(1, 257)]
+    vals += [P - 2**k for k in range(0, 200, 7)] + [rng.randrange(1, 2**rng.randrange(1, 256)) for _ in range(500)]
+    vals += [rng.randrange(1, P) for _ in range(3000)]
+    for a in vals:
+        a %= P
+        if a == 0:
+            continue
+        want = pow(a, -1, P)
+        assert int.from_bytes(call(lib().hfp_op, 3, b32(a), b32(1)), "big") == want, hex(a)
+        assert int.from_bytes(call(lib().hfp_op, 6, b32(a), b32(1)), "big") == want, hex(a)
+    assert int.from_bytes(call(lib().hfp_op, 6, b32(0), b32(1)), "big") == 0
 
 
 def test_montgomery_raw_bound():
