@@ -332,6 +332,13 @@ def test_full_size_c256_schoolbook_sampled():
     _full_size("c256", P.SCHOOLBOOK, 16)
 
 
+@pytest.mark.parametrize("name,path", [("c512", "schoolbook"), ("ml", "schoolbook"), ("c256", "strassen"),
+                                       ("ml", "strassen")])
+def test_full_size_comparison_paths_sampled(name, path):
+    # the comparison paths at BASELINE sizes, sampled outputs vs the Eq. 5 closed form
+    _full_size(name, P.SCHOOLBOOK if path == "schoolbook" else P.STRASSEN, 8)
+
+
 # ------------------------------------------------------------------ edge cases
 def test_empty_and_invalid_sizes():
     z = torch.zeros(0, dtype=torch.uint8, device="cuda")

@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 import synth  # noqa: E402
 from paper_2504_14497_b200 import pcmm as P  # noqa: E402
 
-for name, shape in (("tiny", None), ("c64", (40, 70, 33)), ("ml", (20, 64, 9))):
+for name, shape in (("tiny", None), ("c64", (40, 70, 33)), ("ml", (20, 64, 9)), ("c64", (8, 256, 128))):
     cfg = synth.CONFIGS[name]
     I = synth.make_instance(cfg) if shape is None else synth.make_instance(cfg, m=shape[0], n=shape[1], l=shape[2])
     m, n, l = I.A.shape[0], I.A.shape[1], I.B.shape[1]
