@@ -230,12 +230,36 @@ __device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) {
     for (int k = 0; k < 8; k++) r.v[k] = (T[8 + k] & m) | (t[k] & ~m);
 }
 
+#ifndef PCMM_REDC_FAKE
+#define PCMM_REDC_FAKE 0        // MEASUREMENT ONLY (wrong results): 1 skips the reduction, 2 also the final subtraction
+#endif
 template <int PV>
 __device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
     uint32_t T[16];
     if (PV == 1) fe_prod_eo(T, a, b);
     else fe_prod_os(T, a, b);
+#if PCMM_REDC_FAKE == 2
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = T[8 + k] ^ T[k];
+#elif PCMM_REDC_FAKE == 1
+    uint32_t t[8], m;
+    asm("sub.cc.u32 %0, %9, 0xffffffff;\n\t"
+        "subc.cc.u32 %1, %10, 0xffffffff;\n\t"
+        "subc.cc.u32 %2, %11, 0xffffffff;\n\t"
+        "subc.cc.u32 %3, %12, 0;\n\t"
+        "subc.cc.u32 %4, %13, 0;\n\t"
+        "subc.cc.u32 %5, %14, 0;\n\t"
+        "subc.cc.u32 %6, %15, 1;\n\t"
+        "subc.cc.u32 %7, %16, 0xffffffff;\n\t"
+        "subc.u32 %8, %17, 0;"
+        : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7]), "=r"(m)
+        : "r"(T[8] ^ T[0]), "r"(T[9] ^ T[1]), "r"(T[10] ^ T[2]), "r"(T[11] ^ T[3]), "r"(T[12] ^ T[4]), "r"(T[13] ^ T[5]),
+          "r"(T[14] ^ T[6]), "r"(T[15] ^ T[7]), "r"(0u));
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = ((T[8 + k] ^ T[k]) & m) | (t[k] & ~m);
+#else
     fe_redc_fast(r, T);
+#endif
 }
 
 __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) { fe_mul_fast_v<PCMM_MUL_PRODUCT>(r, a, b); }
