@@ -18,6 +18,8 @@ keys = ["Kernel Name", "gpu__time_duration.sum", "launch__registers_per_thread",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
         "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
         "sm__cycles_elapsed.avg.per_second"]
 for k in keys:
