@@ -18,6 +18,7 @@
 // space (a __grid_constant__ struct: compile-time offsets, so they are constant
 // bank operands of the IMADs and every launch carries its own modulus).
 #include "internal.h"
+#include "paillier_warp.cuh"
 
 namespace pcmm {
 
@@ -267,6 +268,227 @@ __global__ void __launch_bounds__(64) k_pl_school(const __grid_constant__ ModN<L
     st<L>(out + ((int64_t)i * l + j) * L, acc);
 }
 
+// ------------------------------------------------------------ warp-cooperative kernels (L = 32 NL)
+// Same steps as the per-thread kernels above, one warp per residue operation
+// (paillier_warp.cuh): no local-memory ladder registers, ~40 registers per lane.
+template <int NL>
+__device__ __forceinline__ void wmodn(uint32_t n[NL], const ModN<32 * NL> &M, int lane) {
+#pragma unroll
+    for (int j = 0; j < NL; j++) n[j] = M.n[lane * NL + j];
+}
+
+// (v, top) - N when (v, top) >= N; returns the new top
+template <int NL>
+__device__ __forceinline__ uint32_t wsub_top(uint32_t v[NL], uint32_t top, const uint32_t n[NL], int lane) {
+    uint32_t d[NL], b = 0, zero = 0;
+#pragma unroll
+    for (int j = 0; j < NL; j++) {
+        const uint64_t x = (uint64_t)v[j] - n[j] - b;
+        d[j] = (uint32_t)x;
+        b = (uint32_t)(x >> 63);
+        zero |= d[j];
+    }
+    const uint32_t G = __ballot_sync(pw::kFull, b != 0), Pm = __ballot_sync(pw::kFull, b == 0 && zero == 0);
+    uint32_t bout;
+    uint32_t bin = pw::lookahead(G, Pm, lane, &bout);
+#pragma unroll
+    for (int j = 0; j < NL; j++) {
+        const uint64_t x = (uint64_t)d[j] - bin;
+        d[j] = (uint32_t)x;
+        bin = (uint32_t)(x >> 63);
+    }
+    if (top < bout) return top;                              // (v, top) < N: unchanged
+#pragma unroll
+    for (int j = 0; j < NL; j++) v[j] = d[j];
+    return top - bout;
+}
+
+template <int NL>
+__global__ void __launch_bounds__(32) k_plw_setup(const __grid_constant__ ModN<32 * NL> M, uint32_t *__restrict__ one,
+                                                  uint32_t *__restrict__ r2, uint32_t *__restrict__ unit) {
+    constexpr int L = 32 * NL;
+    const int lane = (int)threadIdx.x;
+    uint32_t n[NL], x[NL];
+    wmodn<NL>(n, M, lane);
+#pragma unroll
+    for (int j = 0; j < NL; j++) {
+        x[j] = 0;
+        unit[lane * NL + j] = (lane == 0 && j == 0) ? 1u : 0u;  // plain 1: leaves Montgomery form
+    }
+    uint32_t top = 1;                                        // (x, top) = 2^(32L) = R
+    for (int rep = 0; rep < 8; rep++) {
+        const uint32_t t2 = wsub_top<NL>(x, top, n, lane);
+        if (t2 == top) break;
+        top = t2;
+    }
+    pw::wst<NL>(one, x, lane);                               // R mod N
+    for (int it = 0; it < L / 2; it++) {                     // x <- 2x mod N
+        const uint32_t below = __shfl_up_sync(pw::kFull, x[NL - 1] >> 31, 1);
+        const uint32_t c = __shfl_sync(pw::kFull, x[NL - 1] >> 31, 31);
+#pragma unroll
+        for (int j = NL - 1; j > 0; j--) x[j] = (x[j] << 1) | (x[j - 1] >> 31);
+        x[0] = (x[0] << 1) | (lane == 0 ? 0u : below);
+        pw::wsub_cond<NL>(x, c, n, lane);
+    }
+    for (int sq = 0; sq < 6; sq++) pw::wmont<NL>(x, x, x, n, M.n0, lane);   // 2^(L/2) R -> R^2 (6 squarings)
+    pw::wst<NL>(r2, x, lane);
+}
+
+template <int NL>
+__global__ void __launch_bounds__(128) k_plw_import(const __grid_constant__ ModN<32 * NL> M, const uint32_t *__restrict__ c,
+                                                    int64_t count, const uint32_t *__restrict__ r2,
+                                                    uint32_t *__restrict__ out, int *__restrict__ status) {
+    constexpr int L = 32 * NL;
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = (int)(threadIdx.x & 31);
+    if (e >= count) return;                                  // warp-uniform
+    uint32_t n[NL], x[NL], y[NL], r[NL];
+    wmodn<NL>(n, M, lane);
+    pw::wld<NL>(x, c + e * L, lane);
+#pragma unroll
+    for (int j = 0; j < NL; j++) y[j] = x[j];
+    wsub_top<NL>(y, 0, n, lane);                             // y = x - N iff x >= N (not a residue)
+    uint32_t diff = 0;
+#pragma unroll
+    for (int j = 0; j < NL; j++) diff |= y[j] ^ x[j];
+    if (__any_sync(pw::kFull, diff != 0) && lane == 0) atomicOr(status, kStatusCurve);
+    pw::wld<NL>(r, r2, lane);
+    pw::wmont<NL>(x, x, r, n, M.n0, lane);
+    pw::wst<NL>(out + e * L, x, lane);
+}
+
+// a2 + a3 (Paillier, warp per (k, j)): table [k][j][slot][L], slot 0 = 1 (R mod N)
+template <int NL>
+__global__ void __launch_bounds__(128) k_plw_tables(const __grid_constant__ ModN<32 * NL> M,
+                                                    const uint32_t *__restrict__ bm, const ColPlan *__restrict__ plans,
+                                                    int n_, int l, int N, int S, int maxup, int t,
+                                                    const uint32_t *__restrict__ onep, uint32_t *__restrict__ tables,
+                                                    uint32_t *__restrict__ scr) {
+    constexpr int L = 32 * NL;
+    const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = (int)(threadIdx.x & 31);
+    if (tid >= (int64_t)n_ * l) return;
+    const int k = (int)(tid / l);
+    const ColPlan &pl = plans[k];
+    uint32_t n[NL], one[NL], P[NL], x[NL], y[NL];
+    wmodn<NL>(n, M, lane);
+    pw::wld<NL>(one, onep, lane);
+    pw::wld<NL>(P, bm + tid * L, lane);
+    uint32_t *blk = tables + tid * (int64_t)S * L;
+    uint32_t *sc = scr + tid * (int64_t)2 * maxup * L;
+    pw::wst<NL>(blk, one, lane);                             // slot 0: a_ik = 0 -> 1
+    const int n1 = pl.n[0];
+    if (N == 1) {
+        for (int u = 0; u < n1; u++) {
+            pw::wladder<NL>(x, P, pl.sN[u], t, one, n, M.n0, lane);
+            pw::wst<NL>(blk + (int64_t)(u + 1) * L, x, lane);
+        }
+    } else {
+        int src = 0;
+        for (int u = 0; u < pl.n[N - 1]; u++) {
+            pw::wladder<NL>(x, P, pl.sN[u], t, one, n, M.n0, lane);
+            pw::wst<NL>(sc + (int64_t)u * L, x, lane);
+        }
+        for (int lev = N - 1; lev >= 2; lev--) {             // prefix products, levels N-1 .. 2
+            const int dst = maxup - src;
+            const int nl = pl.n[lev - 1];
+            pw::wld<NL>(x, sc + (int64_t)(src + pl.ptr[lev - 1][0]) * L, lane);
+            pw::wst<NL>(sc + (int64_t)dst * L, x, lane);
+            for (int u = 1; u < nl; u++) {
+                pw::wld<NL>(y, sc + (int64_t)(src + pl.ptr[lev - 1][u]) * L, lane);
+                pw::wmont<NL>(x, x, y, n, M.n0, lane);
+                pw::wst<NL>(sc + (int64_t)(dst + u) * L, x, lane);
+            }
+            src = dst;
+        }
+        pw::wld<NL>(x, sc + (int64_t)(src + pl.ptr[0][0]) * L, lane);   // level 1 -> the table
+        pw::wst<NL>(blk + (int64_t)L, x, lane);
+        for (int u = 1; u < n1; u++) {
+            pw::wld<NL>(y, sc + (int64_t)(src + pl.ptr[0][u]) * L, lane);
+            pw::wmont<NL>(x, x, y, n, M.n0, lane);
+            pw::wst<NL>(blk + (int64_t)(u + 1) * L, x, lane);
+        }
+    }
+    for (int slot = n1 + 1; slot < S; slot++) pw::wst<NL>(blk + (int64_t)slot * L, one, lane);
+}
+
+// a4 (Paillier, warp per (i, j), i fastest)
+template <int NL>
+__global__ void __launch_bounds__(128) k_plw_accum(const __grid_constant__ ModN<32 * NL> M,
+                                                   const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
+                                                   int m, int n_, int l, int S, const uint32_t *__restrict__ onep,
+                                                   const uint32_t *__restrict__ unitp, uint32_t *__restrict__ out) {
+    constexpr int L = 32 * NL;
+    const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = (int)(threadIdx.x & 31);
+    if (tid >= (int64_t)m * l) return;
+    const int i = (int)(tid % m), j = (int)(tid / m);
+    uint32_t n[NL], acc[NL], y[NL];
+    wmodn<NL>(n, M, lane);
+    pw::wld<NL>(acc, onep, lane);
+    for (int k = 0; k < n_; k++) {
+        const int u = rank[(int64_t)k * m + i];
+        if (!u) continue;
+        pw::wld<NL>(y, tables + (((int64_t)k * l + j) * S + u) * L, lane);
+        pw::wmont<NL>(acc, acc, y, n, M.n0, lane);
+    }
+    pw::wld<NL>(y, unitp, lane);
+    pw::wmont<NL>(acc, acc, y, n, M.n0, lane);               // out of Montgomery form
+    pw::wst<NL>(out + ((int64_t)i * l + j) * L, acc, lane);
+}
+
+// s1 (Paillier, warp per (i, j), j fastest): prod_k Alg.4(c_kj, a_ik)
+template <int NL>
+__global__ void __launch_bounds__(128) k_plw_school(const __grid_constant__ ModN<32 * NL> M,
+                                                    const uint8_t *__restrict__ A, int m, int n_, int l, int w,
+                                                    const uint32_t *__restrict__ bm, const uint32_t *__restrict__ onep,
+                                                    const uint32_t *__restrict__ unitp, uint32_t *__restrict__ out,
+                                                    int *__restrict__ status) {
+    constexpr int L = 32 * NL;
+    const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = (int)(threadIdx.x & 31);
+    if (tid >= (int64_t)m * l) return;
+    const int j = (int)(tid % l), i = (int)(tid / l);
+    uint32_t n[NL], one[NL], acc[NL], g[NL], e[NL];
+    wmodn<NL>(n, M, lane);
+    pw::wld<NL>(one, onep, lane);
+    for (int q = 0; q < NL; q++) acc[q] = one[q];
+    bool bad = false;
+    for (int k = 0; k < n_; k++) {
+        const int a = A[(int64_t)i * n_ + k];
+        if (a >= (1 << w)) {
+            bad = true;
+            continue;
+        }
+        if (!a) continue;
+        pw::wld<NL>(g, bm + ((int64_t)k * l + j) * L, lane);
+        pw::wladder<NL>(e, g, a, w, one, n, M.n0, lane);
+        pw::wmont<NL>(acc, acc, e, n, M.n0, lane);
+    }
+    if (bad && lane == 0) atomicOr(status, kStatusBound);
+    pw::wld<NL>(e, unitp, lane);
+    pw::wmont<NL>(acc, acc, e, n, M.n0, lane);
+    pw::wst<NL>(out + ((int64_t)i * l + j) * L, acc, lane);
+}
+
+static int paillier_warp_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PCMM_PAILLIER_WARP");          // measurement override: 0 = one thread per product
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// warp-cooperative kernels for L >= 32 where they win (measured, tools/paillier_prof.py):
+// always at 3072 bits (per-thread L = 96 spills) and for the key setup; at 1024 /
+// 2048 bits only in the latency regime of few independent products (fewer than
+// 32768 warps' worth), where one thread's 32L-long carry chains are the critical path
+inline bool use_warp(int L, int64_t count) {
+    return L >= 32 && paillier_warp_on() && (L >= 96 || count < 32768);
+}
+inline unsigned nbw(int64_t warps) { return (unsigned)((warps + 3) / 4); }
+
 inline unsigned nbp(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 template <int L>
@@ -282,17 +504,35 @@ cudaError_t run_paillier_L(int path, const uint8_t *A, int m, int n, int l, int 
     uint32_t *one = (uint32_t *)(ws + off[0]), *r2 = one + L, *unit = r2 + L;
     uint32_t *bm = (uint32_t *)(ws + off[1]);
     cudaError_t e;
+    const int64_t nl = (int64_t)n * l, ml = (int64_t)m * l;
     prof_begin("pl_setup", s);
-    k_pl_setup<L><<<1, 1, 0, s>>>(M, one, r2, unit);
+    if constexpr (L >= 32) {
+        if (use_warp(L, 1)) k_plw_setup<L / 32><<<1, 32, 0, s>>>(M, one, r2, unit);
+        else k_pl_setup<L><<<1, 1, 0, s>>>(M, one, r2, unit);
+    } else {
+        k_pl_setup<L><<<1, 1, 0, s>>>(M, one, r2, unit);
+    }
     prof_end(s);
     if ((e = cudaGetLastError())) return e;
     prof_begin("pl_import", s);
-    k_pl_import<L><<<nbp((int64_t)n * l, 128), 128, 0, s>>>(M, ctB, (int64_t)n * l, r2, bm, status);
+    if constexpr (L >= 32) {
+        if (use_warp(L, nl)) k_plw_import<L / 32><<<nbw(nl), 128, 0, s>>>(M, ctB, nl, r2, bm, status);
+        else k_pl_import<L><<<nbp(nl, 128), 128, 0, s>>>(M, ctB, nl, r2, bm, status);
+    } else {
+        k_pl_import<L><<<nbp(nl, 128), 128, 0, s>>>(M, ctB, nl, r2, bm, status);
+    }
     prof_end(s);
     if ((e = cudaGetLastError())) return e;
     if (path == 0) {
         prof_begin("pl_school", s);
-        k_pl_school<L><<<nbp((int64_t)m * l, 64), 64, 0, s>>>(M, A, m, n, l, w, bm, one, unit, ctC, status);
+        if constexpr (L >= 32) {
+            if (use_warp(L, ml))
+                k_plw_school<L / 32><<<nbw(ml), 128, 0, s>>>(M, A, m, n, l, w, bm, one, unit, ctC, status);
+            else
+                k_pl_school<L><<<nbp(ml, 64), 64, 0, s>>>(M, A, m, n, l, w, bm, one, unit, ctC, status);
+        } else {
+            k_pl_school<L><<<nbp(ml, 64), 64, 0, s>>>(M, A, m, n, l, w, bm, one, unit, ctC, status);
+        }
         prof_end(s);
         e = cudaGetLastError();
     } else {
@@ -304,11 +544,25 @@ cudaError_t run_paillier_L(int path, const uint8_t *A, int m, int n, int l, int 
         prof_end(s);
         if (e) return e;
         prof_begin("pl_tables", s);
-        k_pl_tables<L><<<nbp((int64_t)n * l, 64), 64, 0, s>>>(M, bm, plans, n, l, N, S, maxup, w, one, tables, scr);
+        if constexpr (L >= 32) {
+            if (use_warp(L, nl))
+                k_plw_tables<L / 32><<<nbw(nl), 128, 0, s>>>(M, bm, plans, n, l, N, S, maxup, w, one, tables, scr);
+            else
+                k_pl_tables<L><<<nbp(nl, 64), 64, 0, s>>>(M, bm, plans, n, l, N, S, maxup, w, one, tables, scr);
+        } else {
+            k_pl_tables<L><<<nbp(nl, 64), 64, 0, s>>>(M, bm, plans, n, l, N, S, maxup, w, one, tables, scr);
+        }
         prof_end(s);
         if ((e = cudaGetLastError())) return e;
         prof_begin("pl_accum", s);
-        k_pl_accum<L><<<nbp((int64_t)m * l, 64), 64, 0, s>>>(M, tables, rank, m, n, l, S, one, unit, ctC);
+        if constexpr (L >= 32) {
+            if (use_warp(L, ml))
+                k_plw_accum<L / 32><<<nbw(ml), 128, 0, s>>>(M, tables, rank, m, n, l, S, one, unit, ctC);
+            else
+                k_pl_accum<L><<<nbp(ml, 64), 64, 0, s>>>(M, tables, rank, m, n, l, S, one, unit, ctC);
+        } else {
+            k_pl_accum<L><<<nbp(ml, 64), 64, 0, s>>>(M, tables, rank, m, n, l, S, one, unit, ctC);
+        }
         prof_end(s);
         e = cudaGetLastError();
     }

@@ -544,6 +544,19 @@ def test_paillier_every_output(nbits, shape, w):
     assert pl.decrypt(n, lam, mu, out[4 * l + 2]) == AB[4, 2]
 
 
+def test_paillier_per_thread_kernels():
+    # the per-thread Paillier kernels (used for large launches at 1024 / 2048 bits) on the same
+    # every-output cases, in a subprocess with the warp-cooperative kernels switched off
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_PAILLIER_WARP="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__,
+                        "-k", "test_paillier_every_output"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_paillier_errors():
     p, q = synth.paillier_primes(512, 256)
     n2 = (p * q) ** 2
