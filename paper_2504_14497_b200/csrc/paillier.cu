@@ -11,7 +11,10 @@
 // rank), level-N exponentiations by Alg. 4, prefix PRODUCTS, and the gather +
 // multiply accumulation.  Plaintexts are non-negative (R20).
 //
-// Arithmetic: one thread per modular product, Montgomery CIOS with R = 2^(32L):
+// Arithmetic, two families with the same memory layout (choice per kernel in
+// run_paillier_L): warp-cooperative products for L >= 32 (paillier_warp.cuh;
+// always at 3072 bits and for the key setup, otherwise for launches of few
+// products) and the original one thread per modular product, Montgomery CIOS with R = 2^(32L):
 // the left operand and the running sum t in registers (inner loops fully
 // unrolled over the L limbs), the right operand streamed from memory one limb
 // per outer step, the modulus and -n^-1 mod 2^32 in the kernel's parameter
