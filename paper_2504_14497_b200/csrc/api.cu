@@ -298,7 +298,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
     const int fast = tables_fast_on() && !is_signed && 2LL * n * l >= 65536 && 2.0 * n * l * L.slots < 4294967296.0;
     LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, is_signed, tables,
-                                            (uint32_t *)(ws + L.scratch), s, fast));
+                                            (uint32_t *)(ws + L.scratch), s, fast, std::min(m, L.slots - 1)));
     uint32_t *atables = (uint32_t *)(ws + L.scratch);
     if (fast) {
         // after k_tables: the affine tables share the region of k_tables' upper-level scratch
@@ -404,8 +404,19 @@ static int mul_wide(int path, const int32_t *A_d, int m, int n, int l, int w, in
     LAUNCH("plan", s, launch_plan_wide(A_d, m, n, w, is_signed, iters, L.cap, pn, psN, pptr, rank, status, s));
     for (int k0 = 0; k0 < n; k0 += L.KC) {
         const int kc = std::min(L.KC, n - k0);
-        LAUNCH("tables", s, launch_tables_wide(bsoa, pn, psN, pptr, n, l, iters, L.cap, L.S, k0, kc, tables, scratch,
-                                               s));
+        // few tables (fewer than two per SM): one CTA per table with block-scan prefix sums
+        static int scan_env = -1;                             // PCMM_WIDE_SCAN: 0 never, 1 auto, 2 always
+        if (scan_env < 0) {
+            const char *e = getenv("PCMM_WIDE_SCAN");
+            scan_env = e ? atoi(e) : 1;
+        }
+        const bool scan = scan_env == 2 || (scan_env == 1 && 2LL * kc * l <= 2LL * num_sms());   // t >= 12: the level-N ECSMs alone are long serial chains
+        if (scan)
+            LAUNCH("tables", s, launch_tables_wide_scan(bsoa, pn, psN, pptr, n, l, iters, L.cap, L.S, k0, kc, tables,
+                                                        scratch, s));
+        else
+            LAUNCH("tables", s, launch_tables_wide(bsoa, pn, psN, pptr, n, l, iters, L.cap, L.S, k0, kc, tables,
+                                                   scratch, s));
         LAUNCH("affine", s, launch_affine(tables, 2LL * kc * l * L.S, scratch, s));
         LAUNCH("accum", s, launch_accum_wide(scratch, rank, m, l, L.S, k0, kc, k0 == 0, out, s));
     }

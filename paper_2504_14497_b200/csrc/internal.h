@@ -40,7 +40,8 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
                         int *status, cudaStream_t s);
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
                           int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s,
-                          int skip_fast = 0);   // skip_fast: consecutive columns left to k_tables_fast
+                          int skip_fast = 0,    // skip_fast: consecutive columns left to k_tables_fast
+                          int maxlen = 0);      // min(m, 2^w - 1): long tables of few launches -> block scan
 // homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
 // plans != nullptr: entries of consecutive columns (built by k_tables_fast) are skipped
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
@@ -104,6 +105,10 @@ cudaError_t launch_plan_wide(const int32_t *A, int m, int n, int w, int is_signe
 cudaError_t launch_tables_wide(const uint32_t *bsoa, const int32_t *pn, const int32_t *psN, const uint16_t *pptr,
                                int n, int l, int N, int cap, int S, int k0, int kc, uint32_t *tables,
                                uint32_t *scratch, cudaStream_t s);
+// few tables (2 kc l small): one CTA per table, block-scan prefix sums (latency)
+cudaError_t launch_tables_wide_scan(const uint32_t *bsoa, const int32_t *pn, const int32_t *psN,
+                                    const uint16_t *pptr, int n, int l, int N, int cap, int S, int k0, int kc,
+                                    uint32_t *tables, uint32_t *scratch, cudaStream_t s);
 cudaError_t launch_accum_wide(const uint32_t *atables, const uint16_t *rank, int m, int l, int S, int k0, int kc,
                               int first, uint32_t *out, cudaStream_t s);
 cudaError_t launch_schoolbook_wide(const int32_t *A, int m, int n, int l, int w, int is_signed,

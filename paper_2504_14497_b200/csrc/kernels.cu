@@ -258,6 +258,120 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
     for (int slot = n1 + 1; slot < S; slot++) table_store(blk, slot, id);
 }
 
+// ------------------------------------------------------------ a2 + a3, few tables: one CTA per table
+// As k_tables for launches with few (c, k, j) tables -- a plaintext vector times one
+// or a few ciphertexts (Tables A7/A8) -- where one thread per table is a
+// serial chain of up to 2^w - 2 complete additions: the level-N ECSMs run in
+// parallel and each level's prefix sum (Alg. 2 l.14-23, any addition order: R7)
+// is a block scan (runs of consecutive elements per thread, Hillis-Steele over
+// the run totals in shared memory, then each run adds its exclusive prefix).
+constexpr int kTScanT = 128;
+
+__device__ __forceinline__ void tsm_store(uint32_t *sm, int i, const pt &q) {
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        sm[(0 * 8 + w) * kTScanT + i] = q.X.v[w];
+        sm[(1 * 8 + w) * kTScanT + i] = q.Y.v[w];
+        sm[(2 * 8 + w) * kTScanT + i] = q.Z.v[w];
+    }
+}
+
+__device__ __forceinline__ void tsm_load(pt &q, const uint32_t *sm, int i) {
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        q.X.v[w] = sm[(0 * 8 + w) * kTScanT + i];
+        q.Y.v[w] = sm[(1 * 8 + w) * kTScanT + i];
+        q.Z.v[w] = sm[(2 * 8 + w) * kTScanT + i];
+    }
+}
+
+__device__ __forceinline__ void table_load(pt &q, const uint32_t *block, int slot) {
+    const uint4 *d = reinterpret_cast<const uint4 *>(block + slot * kPtWords);
+    const uint4 x0 = d[0], x1 = d[1], y0 = d[2], y1 = d[3], z0 = d[4], z1 = d[5];
+    q.X = fe{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
+    q.Y = fe{{y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w}};
+    q.Z = fe{{z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w}};
+}
+
+__global__ void __launch_bounds__(kTScanT) k_tables_scan(const uint32_t *__restrict__ bsoa,
+                                                         const ColPlan *__restrict__ plans, int n, int l, int N, int S,
+                                                         int maxup, uint32_t *__restrict__ tables,
+                                                         uint32_t *__restrict__ scr) {
+    __shared__ uint32_t sm[kPtWords * kTScanT];
+    const int64_t t = blockIdx.x;                                       // table (c, k, j), j fastest
+    const int tid = (int)threadIdx.x;
+    const int j = (int)(t % l);
+    const int k = (int)((t / l) % n);
+    const int c = (int)(t / ((int64_t)l * n));
+    const int64_t cnt = (int64_t)n * l;
+    pt P;
+    soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
+    const ColPlan &pl = plans[k];
+    uint32_t *blk = tables + t * (int64_t)(kPtWords * S);
+    uint32_t *sj = scr + j;
+    const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;
+    pt id;
+    pt_identity(id);
+    const int n1 = pl.n[0];
+    if (tid == 0) table_store(blk, 0, id);
+    for (int slot = n1 + 1 + tid; slot < S; slot += kTScanT) table_store(blk, slot, id);
+    if (N == 1) {
+        for (int u = tid; u < n1; u += kTScanT) {
+            pt e;
+            pt_mul_small_g<MulCall>(e, pl.sN[u], P);                       // Alg. 3 l.5
+            table_store(blk, u + 1, e);
+        }
+        return;
+    }
+    int src = 0;
+    for (int u = tid; u < pl.n[N - 1]; u += kTScanT) {
+        pt e;
+        pt_mul_small_g<MulCall>(e, pl.sN[u], P);                           // Alg. 3 l.5 (v < 0: -(|v| P))
+        scr_store(sj, sbase, src + u, l, e);
+    }
+    __syncthreads();
+    for (int lev = N - 1; lev >= 1; lev--) {                                // levels N-1 .. 1
+        const int nlv = pl.n[lev - 1];
+        const uint8_t *pp = pl.ptr[lev - 1];
+        const int dst = maxup - src;
+        const int E = (nlv + kTScanT - 1) / kTScanT;
+        const int u0 = min(tid * E, nlv), u1 = min(u0 + E, nlv);
+        pt run = id, g;
+        for (int u = u0; u < u1; u++) {                                    // own run, inclusive
+            scr_load(g, sj, sbase, src + pp[u], l);
+            pt_add_nl(run, run, g);
+            if (lev == 1) table_store(blk, u + 1, run);
+            else scr_store(sj, sbase, dst + u, l, run);
+        }
+        tsm_store(sm, tid, run);
+        __syncthreads();
+        for (int d = 1; d < kTScanT; d <<= 1) {                            // Hillis-Steele over run totals
+            pt o;
+            if (tid >= d) tsm_load(o, sm, tid - d);
+            __syncthreads();
+            if (tid >= d) {
+                pt_add_nl(run, run, o);
+                tsm_store(sm, tid, run);
+            }
+            __syncthreads();
+        }
+        if (tid > 0) {
+            pt excl;
+            tsm_load(excl, sm, tid - 1);
+            for (int u = u0; u < u1; u++) {                                // + exclusive prefix
+                pt v;
+                if (lev == 1) table_load(v, blk, u + 1);
+                else scr_load(v, sj, sbase, dst + u, l);
+                pt_add_nl(v, excl, v);
+                if (lev == 1) table_store(blk, u + 1, v);
+                else scr_store(sj, sbase, dst + u, l, v);
+            }
+        }
+        __syncthreads();
+        src = dst;
+    }
+}
+
 // ------------------------------------------------------------ a3': tables -> affine
 // The accumulate loop adds table entries with the XYZZ + affine mixed
 // addition (hot.cu), so the tables are converted once to affine (x, y) =
@@ -961,7 +1075,18 @@ static int tables_fast_enabled() {
 }
 
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s, int fast) {
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s, int fast, int maxlen) {
+    // few tables (fewer than two per SM) of >= 16 entries (maxlen = min(m, 2^w - 1)): one CTA per
+    // table with block-scan prefix sums (measured: at 8-15 entries the serial thread is faster)
+    static int scan_env = -1;                                 // PCMM_TABLES_SCAN: 0 never, 1 auto, 2 always
+    if (scan_env < 0) {
+        const char *e = getenv("PCMM_TABLES_SCAN");
+        scan_env = e ? atoi(e) : 1;
+    }
+    if (!fast && (scan_env == 2 || (scan_env == 1 && maxlen >= 16 && 2LL * n * l <= 2LL * num_sms()))) {
+        k_tables_scan<<<(unsigned)(2LL * n * l), kTScanT, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+        return cudaGetLastError();
+    }
     if (is_signed)
         k_tables<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch,
                                                                     fast);

@@ -241,6 +241,128 @@ __global__ void __launch_bounds__(128, 3) k_tables_wide(const uint32_t *__restri
     for (int slot = n1 + 1; slot < S; slot++) wt_store(blk, slot, id);
 }
 
+// ------------------------------------------------------------ a2 + a3 (wide), few tables: one CTA per table
+// For launches with few tables (a single plaintext vector times one or a few
+// ciphertexts, Tables A7/A8 P:886-949) the one-thread-per-table kernel above is a
+// serial chain of up to cap complete additions per level.  Here a CTA builds one
+// table: the level-N ECSMs in parallel, and each level's prefix sum
+// b^(w)[u] = sum_{v <= u} b^(w+1)[ptr^(w)[v]] (Alg. 2 l.14-23, any addition order:
+// R7) as a block scan: every thread sums its run of consecutive elements, a
+// Hillis-Steele scan over the run totals in shared memory, then each run adds its
+// exclusive prefix -- latency ~ 2 cap / T + log2 T additions instead of cap.
+constexpr int kScanT = 128;
+
+__device__ __forceinline__ void wt_load(pt &q, const uint32_t *block, int slot) {
+    const uint4 *d = reinterpret_cast<const uint4 *>(block + (int64_t)slot * kPtWords);
+    const uint4 x0 = d[0], x1 = d[1], y0 = d[2], y1 = d[3], z0 = d[4], z1 = d[5];
+    q.X = fe{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
+    q.Y = fe{{y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w}};
+    q.Z = fe{{z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w}};
+}
+
+__device__ __forceinline__ void sm_store(uint32_t *sm, int i, const pt &q) {
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        sm[(0 * 8 + w) * kScanT + i] = q.X.v[w];
+        sm[(1 * 8 + w) * kScanT + i] = q.Y.v[w];
+        sm[(2 * 8 + w) * kScanT + i] = q.Z.v[w];
+    }
+}
+
+__device__ __forceinline__ void sm_load(pt &q, const uint32_t *sm, int i) {
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        q.X.v[w] = sm[(0 * 8 + w) * kScanT + i];
+        q.Y.v[w] = sm[(1 * 8 + w) * kScanT + i];
+        q.Z.v[w] = sm[(2 * 8 + w) * kScanT + i];
+    }
+}
+
+__global__ void __launch_bounds__(kScanT) k_tables_wide_scan(const uint32_t *__restrict__ bsoa,
+                                                             const int32_t *__restrict__ pn,
+                                                             const int32_t *__restrict__ psN,
+                                                             const uint16_t *__restrict__ pptr, int n, int l, int N,
+                                                             int cap, int S, int k0, int kc,
+                                                             uint32_t *__restrict__ tables,
+                                                             uint32_t *__restrict__ scr) {
+    __shared__ uint32_t sm[kPtWords * kScanT];
+    const int64_t t = blockIdx.x;                                       // table (c, kk, j), j fastest
+    const int tid = (int)threadIdx.x;
+    const int j = (int)(t % l);
+    const int kk = (int)((t / l) % kc);
+    const int c = (int)(t / ((int64_t)l * kc));
+    const int k = k0 + kk;
+    const int64_t cnt = (int64_t)n * l;
+    pt P;
+    w_soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
+    const int32_t *nl = pn + (int64_t)k * 4;
+    const int32_t *sN = psN + (int64_t)k * cap;
+    const uint16_t *ptr = pptr + (int64_t)k * 3 * cap;
+    uint32_t *blk = tables + t * (int64_t)S * kPtWords;
+    uint32_t *sj = scr + j;
+    const int64_t sbase = ((int64_t)c * kc + kk) * 2 * cap * kPtWords;
+    pt id;
+    pt_identity(id);
+    const int n1 = nl[0];
+    if (tid == 0) wt_store(blk, 0, id);
+    for (int slot = n1 + 1 + tid; slot < S; slot += kScanT) wt_store(blk, slot, id);
+    if (N == 1) {
+        for (int u = tid; u < n1; u += kScanT) {
+            pt e;
+            pt_mul_small_g<MulCall>(e, sN[u], P);                           // Alg. 3 l.5
+            wt_store(blk, u + 1, e);
+        }
+        return;
+    }
+    int src = 0;
+    for (int u = tid; u < nl[N - 1]; u += kScanT) {
+        pt e;
+        pt_mul_small_g<MulCall>(e, sN[u], P);                               // Alg. 3 l.5
+        ws_store(sj, sbase, src + u, l, e);
+    }
+    __syncthreads();
+    for (int lev = N - 1; lev >= 1; lev--) {                                // levels N-1 .. 1
+        const int nlv = nl[lev - 1];
+        const uint16_t *pl = ptr + (int64_t)(lev - 1) * cap;
+        const int dst = cap - src;
+        const int E = (nlv + kScanT - 1) / kScanT;
+        const int u0 = min(tid * E, nlv), u1 = min(u0 + E, nlv);
+        pt run = id, g;
+        for (int u = u0; u < u1; u++) {                                    // own run, inclusive
+            ws_load(g, sj, sbase, src + pl[u], l);
+            pt_add_nl(run, run, g);
+            if (lev == 1) wt_store(blk, u + 1, run);
+            else ws_store(sj, sbase, dst + u, l, run);
+        }
+        sm_store(sm, tid, run);
+        __syncthreads();
+        for (int d = 1; d < kScanT; d <<= 1) {                             // Hillis-Steele over run totals
+            pt o;
+            if (tid >= d) sm_load(o, sm, tid - d);
+            __syncthreads();
+            if (tid >= d) {
+                pt_add_nl(run, run, o);
+                sm_store(sm, tid, run);
+            }
+            __syncthreads();
+        }
+        pt excl = id;
+        if (tid > 0) sm_load(excl, sm, tid - 1);
+        if (tid > 0) {
+            for (int u = u0; u < u1; u++) {                                // + exclusive prefix
+                pt v;
+                if (lev == 1) wt_load(v, blk, u + 1);
+                else ws_load(v, sj, sbase, dst + u, l);
+                pt_add_nl(v, excl, v);
+                if (lev == 1) wt_store(blk, u + 1, v);
+                else ws_store(sj, sbase, dst + u, l, v);
+            }
+        }
+        __syncthreads();
+        src = dst;
+    }
+}
+
 // ------------------------------------------------------------ s1 (wide): schoolbook with int32 plaintexts
 __global__ void __launch_bounds__(128) k_school_wide(const int32_t *__restrict__ A, int m, int n, int l, int w,
                                                      int is_signed, const uint32_t *__restrict__ bsoa,
@@ -295,6 +417,14 @@ cudaError_t launch_tables_wide(const uint32_t *bsoa, const int32_t *pn, const in
                                uint32_t *scratch, cudaStream_t s) {
     k_tables_wide<<<wblocks(2LL * kc * l, 128), 128, 0, s>>>(bsoa, pn, psN, pptr, n, l, N, cap, S, k0, kc, tables,
                                                             scratch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tables_wide_scan(const uint32_t *bsoa, const int32_t *pn, const int32_t *psN,
+                                    const uint16_t *pptr, int n, int l, int N, int cap, int S, int k0, int kc,
+                                    uint32_t *tables, uint32_t *scratch, cudaStream_t s) {
+    k_tables_wide_scan<<<(unsigned)(2LL * kc * l), kScanT, 0, s>>>(bsoa, pn, psN, pptr, n, l, N, cap, S, k0, kc,
+                                                                   tables, scratch);
     return cudaGetLastError();
 }
 

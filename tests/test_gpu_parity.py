@@ -607,8 +607,44 @@ def test_paillier_3072_64cube_sampled():
 @pytest.mark.parametrize("t", [4, 12])
 def test_vector_times_ciphertext_scalars(t):
     # NEXT-1's vector workload (Tables A7/A8): an n x 1 plaintext vector times a 1 x l row of ciphertexts
-    m, l = 37, 5
-    cfg = synth.Config("vec", m, 1, l, t, False, 0, 255, 900 + t)
+    _vector_case(37, 5, t)
+
+
+@pytest.mark.parametrize("m,l,t", [(300, 3, 16), (1000, 1, 16), (700, 2, 12)])
+def test_vector_long_tables_block_scan(m, l, t):
+    # few tables with hundreds of entries: the wide path's one-CTA-per-table block-scan kernel
+    # (runs of several entries per thread, a 128-wide scan of run totals)
+    _vector_case(m, l, t)
+
+
+def test_wide_block_scan_forced():
+    # the block-scan table kernel on the every-output wide cases (PCMM_WIDE_SCAN=2 forces it)
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_WIDE_SCAN="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__,
+                        "-k", "test_wide_every_output or test_wide_chunked"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_byte_block_scan_forced():
+    # the byte path's block-scan table kernel (k_tables_scan) forced on the every-output cases
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_TABLES_SCAN="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or "
+                        "test_accumulator_exceptional or test_vector_times"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _vector_case(m, l, t):
+    cfg = synth.Config("vec", m, 1, l, t, False, 0, 255, 900 + t + m)
     I = synth.make_instance(cfg)
     x = synth.keygen_secret(cfg.seed)
     ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be)
