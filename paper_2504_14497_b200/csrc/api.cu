@@ -296,17 +296,15 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
     // consecutive-column tables (k_tables_fast): unsigned A, launches that fill the GPU
     // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
-    const int fast = tables_fast_on() && !is_signed && 2LL * n * l >= 65536 && 2.0 * n * l * L.slots < 4294967296.0;
+    const int fast = tables_fast_on() && !is_signed && 2LL * n * l >= 65536;
     LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, is_signed, tables,
                                             (uint32_t *)(ws + L.scratch), s, fast, std::min(m, L.slots - 1)));
     uint32_t *atables = (uint32_t *)(ws + L.scratch);
     if (fast) {
         // after k_tables: the affine tables share the region of k_tables' upper-level scratch
         LAUNCH("tables_fast", s, launch_tables_fast(bsoa, plans, n, l, iters, L.slots, tables, atables, s));
-        LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s, plans, n, l, L.slots, iters));
-    } else {
-        LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s));
     }
+    LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s, plans, n, l, L.slots, iters, fast));
     const int64_t cnt = (int64_t)m * l;
     uint32_t *acc_out = L.ksplit == 1 ? out : (uint32_t *)(ws + L.partial);
     const int64_t split_stride = L.ksplit == 1 ? 0 : 2LL * kPtWords * cnt;

@@ -44,8 +44,10 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
                           int maxlen = 0);      // min(m, 2^w - 1): long tables of few launches -> block scan
 // homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
 // plans != nullptr: entries of consecutive columns (built by k_tables_fast) are skipped
+// plans != nullptr (byte path): per-column entry kinds (slot 0 / unused slots -> identity markers without
+// reading the tables; fast != 0: consecutive columns come from k_tables_fast)
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
-                          const ColPlan *plans = nullptr, int n = 0, int l = 0, int S = 0, int N = 0);
+                          const ColPlan *plans = nullptr, int n = 0, int l = 0, int S = 0, int N = 0, int fast = 0);
 // consecutive columns (s^(1) = {1..n1}): XYZZ prefix sums + fused affine conversion
 // (k_tables_fast); k_tables skips them when tables_fast_on()
 int tables_fast_on();

@@ -210,10 +210,7 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
     uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
     uint32_t *sj = scr + j;
     const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;   // in units of l-strided words
-    pt id;
-    pt_identity(id);
-    table_store(blk, 0, id);
-    const int n1 = pl.n[0];
+    const int n1 = pl.n[0];                  // slot 0 and slots > n1: identity markers written by k_affine
     if (N == 1) {
         for (int u = 0; u < n1; u++) {                                      // Alg. 3 line 5 only
             pt e;
@@ -255,7 +252,6 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
             table_store(blk, u + 1, run);
         }
     }
-    for (int slot = n1 + 1; slot < S; slot++) table_store(blk, slot, id);
 }
 
 // ------------------------------------------------------------ a2 + a3, few tables: one CTA per table
@@ -486,7 +482,7 @@ __device__ __forceinline__ fe cta_inverse(const fe &acc, fe *wtot, fe *winv) {
 // consecutive column (k_tables_fast), slots 2..n1 hold XYZZ (X, Y, ZZ in the
 // projective slot, ZZZ in the x half of the affine slot: 1/ZZZ from the batch,
 // 1/Z = ZZ/ZZZ, x = X/Z^2, y = Y/ZZZ) and the other slots are already final.
-enum { kAffSkip = 0, kAffProj = 1, kAffXyzz = 2 };
+enum { kAffSkip = 0, kAffProj = 1, kAffXyzz = 2, kAffInf = 3 };   // kAffInf: slot 0 / unused slot of a k_tables column
 #ifndef PCMM_TFAST_PROJ
 #define PCMM_TFAST_PROJ 0       // 1: k_tables_fast stores homogeneous (X ZZZ : Y ZZ : ZZ ZZZ) entries instead
 #endif
@@ -521,7 +517,7 @@ __device__ __forceinline__ void aff_fetch(AffEnt &a, const uint32_t *__restrict_
                                           const uint32_t *__restrict__ atab, int64_t e, int kind) {
     a.kind = kind;
     a.ok = false;
-    if (kind == kAffSkip) return;
+    if (kind == kAffSkip || kind == kAffInf) return;
     const uint4 *src = reinterpret_cast<const uint4 *>(tab + e * kPtWords);
     const uint4 x0 = src[0], x1 = src[1], y0 = src[2], y1 = src[3], z0 = src[4], z1 = src[5];
     a.X = fe{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
@@ -545,21 +541,24 @@ template <bool kFermat>
 __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t *__restrict__ tab, int64_t entries,
                                                                   int batch, uint32_t *__restrict__ atab,
                                                                   const ColPlan *__restrict__ plans, int n, int l,
-                                                                  int S, int N) {
+                                                                  int S, int N, int fast) {
     __shared__ fe wtot[4], winv[4];
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // entry e = ((c n + k) l + j) S + slot; plans != nullptr only on the byte path
-    // (entries = 2 n l S < 2^32, S a power of two): 32-bit index arithmetic
+    // entry e = ((c n + k) l + j) S + slot, S a power of two; plans != nullptr only on the byte path;
+    // 32-bit index arithmetic when entries < 2^32
     const uint32_t sl = (uint32_t)S * (uint32_t)l;
+    const bool small = entries < (1LL << 32);
     auto kind = [&](int64_t e) -> int {
         if (e >= entries) return kAffSkip;
         if (plans == nullptr) return kAffProj;
         const uint32_t e32 = (uint32_t)e;
-        const ColPlan &pl = plans[(e32 / sl) % (uint32_t)n];
-        if (!col_consecutive(pl, N)) return kAffProj;
-        const int slot = (int)(e32 & (uint32_t)(S - 1));
-        return (slot >= 2 && slot <= pl.n[0]) ? (PCMM_TFAST_PROJ ? kAffProj : kAffXyzz) : kAffSkip;
+        const ColPlan &pl = plans[small ? (e32 / sl) % (uint32_t)n : (int)((e / ((int64_t)S * l)) % n)];
+        const int slot = (int)(e & (int64_t)(S - 1));
+        if (fast && col_consecutive(pl, N))
+            return (slot >= 2 && slot <= pl.n[0]) ? (PCMM_TFAST_PROJ ? kAffProj : kAffXyzz) : kAffSkip;
+        // k_tables leaves slot 0 and the unused slots unwritten: the identity marker is written here
+        return (slot >= 1 && slot <= pl.n[0]) ? kAffProj : kAffInf;
     };
     fe one;
     fe_one_mont(one);
@@ -570,6 +569,10 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
         if (e >= entries) break;
         const int kd = kind(e);
         if (kd == kAffSkip) continue;
+        if (kd == kAffInf) {
+            st_aff_inf(atab + e * kAffWords);
+            continue;
+        }
         const AffIn a0 = kd == kAffProj ? aff_load_z(tab, e, entries) : aff_load_zzz(atab, e);
         if (kd == kAffProj) {
             aff_pass1_store(atab, e, entries, a0, acc);
@@ -1032,7 +1035,7 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
 }
 
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
-                          const ColPlan *plans, int n, int l, int S, int N) {
+                          const ColPlan *plans, int n, int l, int S, int N, int fast) {
     if (entries <= 0) return cudaSuccess;
     // up to 32 entries per lane (one inversion per 4096 entries), fewer when that
     // would leave fewer than ~4 warps per SM (256^3: batch 32 0.48 ms, 16 0.55, 8 0.76)
@@ -1059,9 +1062,11 @@ cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *ata
     // with the one-wave batch and 128 registers (PCMM_AFFINE_MINB) divsteps win everywhere:
     // 256^3 0.309 vs 0.324 ms, 512^3 0.299 vs 0.314, ML 0.246 vs 0.261, 64^3 0.091 vs 0.107
     if (inv_env == 1)
-        k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
+        k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N,
+                                                                  fast);
     else
-        k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N);
+        k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N,
+                                                                   fast);
     return cudaGetLastError();
 }
 
