@@ -121,6 +121,25 @@ def algorithmic_counts(A: np.ndarray, l: int, w: int):
     return acc_adds, tbl_adds, tbl_dbls
 
 
+def paper_model_adds(A: np.ndarray, l: int, w: int) -> int:
+    """The paper's cost model for the Cussen run (SURVEY.md §8(c) counts; Table A6 form):
+    per column k, l x (4 t |s^(N)_k| + 2 sum_{w<N} |s^(w)_k|) equivalent point additions (an ECSM of width
+    t = w is t additions + t doublings per component) plus the dense accumulation 2 m l (n - 1)."""
+    m, n = A.shape
+    tot = 2 * m * l * (n - 1)
+    for k in range(n):
+        v = A[:, k].astype(np.int64)
+        sizes = []
+        for lev in range(4):
+            s = np.unique(v)
+            s = s[s != 0]
+            sizes.append(len(s))
+            if lev < 3:
+                v = np.diff(np.concatenate([[0], s]))
+        tot += l * (4 * w * sizes[3] + 2 * sum(sizes[:3]))
+    return tot
+
+
 def table_entries(A: np.ndarray, l: int) -> int:
     """Non-identity table entries (distinct nonzero values per column x 2 l)."""
     return 2 * l * sum(len(np.setdiff1d(np.unique(A[:, k]), [0])) for k in range(A.shape[1]))
@@ -429,6 +448,7 @@ def main():
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(cfg, args.path, world),
         "point_adds_per_s": world * (acc_adds + tbl_adds + tbl_dbls) / (ms * 1e-3),
+        "paper_model_adds_per_s": world * paper_model_adds(I.A, l, w) / (ms * 1e-3),
         "fp_mul_per_s": world * F_total / (ms * 1e-3),
         "roofline_whole_step": {"achieved": F_total / (ms * 1e-3) / 1e9, "peak": peak_fpmul,
                                 "frac": F_total / (ms * 1e-3) / 1e9 / peak_fpmul, "unit": "G fp_mul/s"},

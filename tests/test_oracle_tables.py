@@ -76,3 +76,21 @@ def test_oracle_run_counts_follow_model():
     _, (adds_c, dbls_c, ecsm_c, bits_c) = oracle.pcmm(oracle.CUSSEN, I.A, ct, 8, 2)
     n_mults = sum(oracle.cussen_counts(I.A[:, k].astype(np.int64))[0] for k in range(8))
     assert ecsm_c == 2 * 8 * n_mults
+
+
+def test_bench_counts_match_oracle_compression():
+    # bench.py's host-side work counts (the roofline numerator's table ops and the paper-model
+    # equivalent additions it reports) agree with the oracle's Alg. 2 compression of every column
+    import bench
+    import synth
+    for name in ("tiny", "c64", "ml"):
+        cfg = synth.CONFIGS[name]
+        I = synth.make_instance(cfg) if name != "ml" else synth.make_instance(cfg, m=32, n=48, l=5)
+        m, n = I.A.shape
+        l = I.B.shape[1]
+        levels = [oracle.cussen_counts(I.A[:, k])[3] for k in range(n)]
+        assert bench.paper_model_adds(I.A, l, cfg.w) == oracle.paper_model_equiv_adds_cussen(levels, cfg.w, m, n, l)
+        # executed prefix additions: sum over levels w < N of (|s^(w)| - 1), per (k, j, c)
+        _, tbl_adds, _ = bench.algorithmic_counts(I.A, l, cfg.w)
+        exec_prefix = 2 * l * sum(max(lv[w] - 1, 0) for lv in levels for w in range(3))
+        assert tbl_adds >= exec_prefix
