@@ -674,6 +674,142 @@ __device__ __forceinline__ void ld_fe2(fe &a, fe &b, const uint32_t *d) {
 }
 
 
+// ------------------------------------------------------------ a2 + a3 for 2^w >= 128 slots: XYZZ level 1
+// As k_tables (levels N .. 2 identical, projective), then the level-2 entries --
+// the only addends of the level-1 prefix sum (Alg. 2 l.14-23), a handful of small
+// multiples v P -- are made affine with one batch inversion shared by the warp
+// (lane products of their Z, prefix / suffix products by shuffles, one fe_inv of
+// the warp total run by all lanes), and the level-1 prefix sum, up to 2^w - 2
+// additions, runs as XYZZ mixed additions (8M + 2S instead of 12M + 2m_b).  Its
+// entries are converted to homogeneous coordinates (3M) for k_affine.
+template <bool kSigned>
+__global__ void __launch_bounds__(128, PCMM_TABLES_MINB)
+    k_tables_x(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans, int n, int l, int N, int S,
+               int maxup, uint32_t *__restrict__ tables, uint32_t *__restrict__ scr, int skip_fast) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = (int)(threadIdx.x & 31);
+    const int64_t total = 2LL * n * l;
+    bool valid = t < total;
+    const int64_t tt = valid ? t : total - 1;
+    const int j = (int)(tt % l);
+    const int k = (int)((tt / l) % n);
+    const int c = (int)(tt / ((int64_t)l * n));
+    const int64_t cnt = (int64_t)n * l;
+    const ColPlan &pl = plans[k];
+    if (skip_fast && col_consecutive(pl, N)) valid = false;          // k_tables_fast
+    uint32_t *sj = scr + j;
+    const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;
+    int src = 0, n2 = 0;
+    if (valid) {
+        pt P;
+        soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
+        const int nN = pl.n[N - 1];
+        if (kSigned) {
+            level_n_products_shared(pl.sN, nN, P, sj, sbase, l, src);
+        } else {
+            for (int u = 0; u < nN; u++) {
+                pt e;
+                pt_mul_small_g<MulCall>(e, pl.sN[u], P);
+                scr_store(sj, sbase, src + u, l, e);
+            }
+        }
+        for (int lev = N - 1; lev >= 2; lev--) {                        // prefix sums, levels N-1 .. 2
+            const int dst = maxup - src;
+            const int nl = pl.n[lev - 1];
+            pt run, g;
+            scr_load(run, sj, sbase, src + pl.ptr[lev - 1][0], l);
+            scr_store(sj, sbase, dst, l, run);
+            for (int u = 1; u < nl; u++) {
+                scr_load(g, sj, sbase, src + pl.ptr[lev - 1][u], l);
+                pt_add_pair(run, run, g);
+                scr_store(sj, sbase, dst + u, l, run);
+            }
+            src = dst;
+        }
+        n2 = pl.n[1];
+    }
+    // level-2 entries -> affine: prefix products parked in the Z words of the other buffer
+    const int dst = maxup - src;
+    auto zword = [&](int e, int q) -> uint32_t * { return sj + (sbase + (int64_t)e * kPtWords + 16 + q) * l; };
+    fe one;
+    fe_one_mont(one);
+    fe acc = one;
+    for (int u = 0; u < n2; u++) {
+        fe z;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            z.v[q] = *zword(src + u, q);
+            *zword(dst + u, q) = acc.v[q];
+        }
+        if (!fe_is_zero(z)) fe_mul(acc, acc, z);
+    }
+    fe Q = acc, Sx = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const fe q = fe_shfl_up(Q, d), sv = fe_shfl_down(Sx, d);
+        fe qm, sm;
+        fe_mul(qm, Q, q);
+        fe_mul(sm, Sx, sv);
+        if (lane >= d) Q = qm;
+        if (lane + d < 32) Sx = sm;
+    }
+    fe tot, inv;
+#pragma unroll
+    for (int i = 0; i < 8; i++) tot.v[i] = __shfl_sync(0xffffffffu, Q.v[i], 31);
+    fe qprev = fe_shfl_up(Q, 1), snext = fe_shfl_down(Sx, 1);
+    if (lane == 0) qprev = one;
+    if (lane == 31) snext = one;
+    fe_inv(inv, tot);                                                   // one inversion per warp
+    fe_mul(inv, inv, qprev);
+    fe_mul(inv, inv, snext);                                            // 1 / (this lane's product)
+    for (int u = n2 - 1; u >= 0; u--) {
+        pt e;
+        scr_load(e, sj, sbase, src + u, l);
+        fe pre, x, y, zi;
+#pragma unroll
+        for (int q = 0; q < 8; q++) pre.v[q] = *zword(dst + u, q);
+        uint32_t *ex = sj + (sbase + (int64_t)(dst + u) * kPtWords) * l;   // affine (x, y) in words 0..15
+        if (fe_is_zero(e.Z)) {                                          // the identity (P = identity)
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                ex[q * l] = 0xffffffffu;
+                ex[(8 + q) * l] = 0;
+            }
+            continue;
+        }
+        fe_mul(zi, inv, pre);
+        fe_mul(inv, inv, e.Z);
+        fe_mul(x, e.X, zi);
+        fe_mul(y, e.Y, zi);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            ex[q * l] = x.v[q];
+            ex[(8 + q) * l] = y.v[q];
+        }
+    }
+    if (!valid) return;
+    // level 1: XYZZ prefix sum of the affine level-2 entries (gathered by tracking pointer), each
+    // entry stored homogeneous (X ZZZ : Y ZZ : ZZ ZZZ) for k_affine (the affine slots overlap other
+    // tables' upper-level scratch while this kernel runs, so nothing is parked there)
+    const int n1 = pl.n[0];
+    uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
+    xyzz run;
+    xyzz_init(run);
+    for (int u = 0; u < n1; u++) {
+        const uint32_t *ex = sj + (sbase + (int64_t)(dst + pl.ptr[0][u]) * kPtWords) * l;
+        fe x, y;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            x.v[q] = ex[q * l];
+            y.v[q] = ex[(8 + q) * l];
+        }
+        xyzz_add_aff(run, x, y);
+        pt h;
+        xyzz_to_proj(h, run);                                           // the identity: Z = 0
+        table_store(blk, u + 1, h);
+    }
+}
+
 #ifndef PCMM_TFAST_MINB
 #define PCMM_TFAST_MINB 3
 #endif
@@ -1091,6 +1227,20 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
     }
     if (!fast && (scan_env == 2 || (scan_env == 1 && maxlen >= 16 && 2LL * n * l <= 2LL * num_sms()))) {
         k_tables_scan<<<(unsigned)(2LL * n * l), kTScanT, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch);
+        return cudaGetLastError();
+    }
+    static int x_env = -1;                                    // PCMM_TABLES_XYZZ: 0 off, 1 for 2^w >= 128 slots
+    if (x_env < 0) {
+        const char *e = getenv("PCMM_TABLES_XYZZ");
+        x_env = e ? atoi(e) : 1;
+    }
+    if (x_env && slots >= 128 && N >= 2) {    // w = 8, 256^3: 4.49 -> 4.31 ms; w = 6: 3 % slower
+        if (is_signed)
+            k_tables_x<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables,
+                                                                          scratch, fast);
+        else
+            k_tables_x<false><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables,
+                                                                           scratch, fast);
         return cudaGetLastError();
     }
     if (is_signed)
