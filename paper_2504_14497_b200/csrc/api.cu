@@ -75,9 +75,17 @@ Layout layout(int m, int n, int l, int w, int path) {
         L.maxup = max_upper(w);
         const double resident =
             (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(L.slots) : accum_global_ctas_per_sm());
+        // On the shared-memory path only splits whose k-range is a whole number of table chunks
+        // are considered when there are any besides 1 (measured: 256^3 2 splits 4.306 ms vs 3 ragged
+        // ones 4.323, 512^3 4 splits 24.50 vs 3: 24.88, ML 16 splits 2.88 vs 10: 2.92).
+        const int kch = w <= 4 ? accum_chunk(L.slots) : 0;
+        bool any_aligned = false;
+        for (int cand = 2; cand <= 16 && cand <= n && kch && n >= 4 * kch; cand++)   // (64^3: latency regime)
+            if (n % (cand * kch) == 0) any_aligned = true;
         int ks = 1;
         double best = 1e30;
         for (int cand = 1; cand <= 16 && cand <= n; cand++) {
+            if (any_aligned && cand > 1 && n % (cand * kch) != 0) continue;
             const double waves = std::ceil((double)base * cand / resident);
             const double cost = waves / cand * (1.0 + 0.01 * (cand - 1)) + (n / cand < 8 ? 1.0 : 0.0);
             if (cost < best - 1e-9) { best = cost; ks = cand; }

@@ -350,6 +350,15 @@ int accum_ctas_per_sm(int slots) {
 
 int accum_rows() { return AccumCfg<16>::kRows; }
 
+int accum_chunk(int slots) {
+    switch (slots) {
+        case 2: return AccumCfg<2>::kChunk;
+        case 4: return AccumCfg<4>::kChunk;
+        case 8: return AccumCfg<8>::kChunk;
+        default: return AccumCfg<16>::kChunk;
+    }
+}
+
 template <int S>
 static cudaError_t launch_accum_s(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int ksplit,
                                   uint32_t *out, int64_t stride, cudaStream_t s) {

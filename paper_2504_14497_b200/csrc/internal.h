@@ -116,5 +116,6 @@ cudaError_t launch_accum_wide(const uint32_t *atables, const uint16_t *rank, int
 cudaError_t launch_schoolbook_wide(const int32_t *A, int m, int n, int l, int w, int is_signed,
                                    const uint32_t *bsoa, uint32_t *out, int *status, cudaStream_t s);
 int accum_rows();
+int accum_chunk(int slots);   // k per shared-memory table chunk of k_accum (2^w <= 16 slots)
 
 }  // namespace pcmm
