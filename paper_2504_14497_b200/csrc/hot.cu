@@ -46,15 +46,37 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #endif
 #endif
 
+#ifndef PCMM_ACC_ROWS
+#define PCMM_ACC_ROWS 128       // rows of A (threads) per k_accum CTA
+#endif
+#ifndef PCMM_ACC_EW
+#define PCMM_ACC_EW 17          // shared-memory words per 16-word table entry (17: odd stride; 20: 16-B vector loads)
+#endif
 template <int S>
 struct AccumCfg {
-    static constexpr int kRows = 128;
+    static constexpr int kRows = PCMM_ACC_ROWS;
     static constexpr int kChunk = (PCMM_ACCUM_CHUNK_SLOTS / S) < 128 ? (PCMM_ACCUM_CHUNK_SLOTS / S) : 128;
     static constexpr int kTW = kAffWords * S;                      // words per table (global, entry-major)
-    static constexpr int kEW = kAffWords + 1;                      // shared-memory entry stride (odd: no conflicts)
+    static constexpr int kEW = PCMM_ACC_EW;                        // shared-memory entry stride
     static constexpr int kTWs = kEW * S;                           // words per table in shared memory
     static constexpr size_t kSmem = (size_t)kChunk * kTWs * 4 + (size_t)kChunk * kRows;
 };
+
+template <int EW>
+__device__ __forceinline__ void ld_entry(fe &x, fe &y, const uint32_t *T) {
+    if constexpr (EW % 4 == 0) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(T);
+        const uint4 a = q[0], b = q[1], c = q[2], d = q[3];
+        x = fe{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+        y = fe{{c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w}};
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            x.v[q] = T[q];
+            y.v[q] = T[8 + q];
+        }
+    }
+}
 
 // Stage one k-chunk: tables and the rank bytes of the CTA's rows.  Out of line so
 // that the staging code does not perturb the hot loop's register allocation.
@@ -113,25 +135,14 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
         if (kk < kc) {
             fe x2, y2, U2;
             bool have_u2 = false;
-            {
-                const uint32_t *T = tsm + kk * TWS + rsm[kk * ROWS + tid] * EW;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    x2.v[q] = T[q];
-                    y2.v[q] = T[8 + q];
-                }
-            }
+            ld_entry<EW>(x2, y2, tsm + kk * TWS + rsm[kk * ROWS + tid] * EW);
             while (true) {
                 int kn = kk + 1;
                 while (kn < kc && rsm[kn * ROWS + tid] == 0) kn++;
                 const bool more = kn < kc;
                 const uint32_t *T = tsm + (more ? kn * TWS + rsm[kn * ROWS + tid] * EW : kk * TWS + rsm[kk * ROWS + tid] * EW);
                 fe xn, yn;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    xn.v[q] = T[q];
-                    yn.v[q] = T[8 + q];
-                }
+                ld_entry<EW>(xn, yn, T);
                 xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);
                 if (!more) break;
                 x2 = xn;
