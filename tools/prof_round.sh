@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round profiling pass (run under gpurun, 1 GPU): smoke, plain bench, launch list,
-# one `ncu --set full` capture each of k_accum, k_tables and k_affine on the c256 bench.
+# one `ncu --set full` capture each of k_accum, k_tables_fast and k_affine on the c256 bench.
 CMD="python bench.py --config c256 --steps 2 --warmup 1 --no-cpu-baseline --no-schoolbook"
 mkdir -p gpurun_out
 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
