@@ -246,6 +246,25 @@ def test_consecutive_column_tables_mixed(w):
     assert (_gpu_pcmm(A, ct, l, w, False, P.CUSSEN) == exp).all()
 
 
+@pytest.mark.parametrize("w,signed", [(8, False), (7, True)])
+def test_xyzz_level1_tables_with_identities(w, signed):
+    # k_tables_x (2^w >= 128 slots, many tables): level-2 entries made affine by a warp-shared inversion,
+    # level-1 prefix sums as XYZZ mixed additions; identity ciphertexts (both or one component) and
+    # repeated ciphertexts in the inputs
+    m, n, l = 40, 24, 16
+    cfg = synth.Config("x", m, n, l, w, signed, 0, 255, 300 + w)
+    I = synth.make_instance(cfg)
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct[3, 2] = 0                                         # (inf, inf)
+    ct[5, :4, :64] = 0                                   # C1 = inf
+    ct[7] = ct[6]                                        # equal ciphertexts in consecutive k
+    ct = np.ascontiguousarray(ct.reshape(n * l, 128))
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, l, w)
+    for path in (P.CUSSEN, P.SCHOOLBOOK):
+        assert (_gpu_pcmm(I.A, ct, l, w, signed, path) == exp).all(), path
+
+
 @pytest.mark.parametrize("w", [4, 6])
 def test_accumulator_exceptional_cases(w):
     # Equal ciphertexts in rows k = 0..3 make the accumulated sum equal to +-(the next
