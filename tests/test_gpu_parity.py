@@ -421,7 +421,8 @@ def test_strassen_c64_every_output():
 
 # ------------------------------------------------------------------ NEXT-1: wide plaintexts (t = 12, 16)
 @pytest.mark.parametrize("shape,t,signed", [((20, 24, 6), 12, False), ((33, 17, 5), 16, False),
-                                            ((16, 40, 3), 16, True), ((64, 64, 64), 16, False)])
+                                            ((16, 40, 3), 16, True), ((64, 64, 64), 16, False),
+                                            ((40, 48, 8), 12, True)])
 def test_wide_every_output(shape, t, signed):
     # the paper's t = 12, 16 grid (Table A9): int32 plaintexts, up to min(m, 2^t - 1)
     # distinct values per column; unsigned 16-bit values above 2^15 included
