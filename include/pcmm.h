@@ -94,7 +94,11 @@ PCMM_API int pcmm_keygen(uint64_t seed, uint8_t sk_h[32], uint8_t pk_h[64]);
  *   r_d  : uint8[count][32] big-endian randomness, each in [1, q-1] (caller's
  *          responsibility; values are used as given).
  *   ct_d : uint8[count][128] canonical ciphertexts (output).
- * Errors: EINVAL (null / count < 0), ENOTONCURVE (pk not on curve), ECUDA. */
+ * Checks (host, before any launch): pk is the canonical encoding of a P-256
+ *   point (x, y < p, y^2 = x^3 - 3x + b; the identity is rejected), r_d and
+ *   ct_d are 16-byte aligned.
+ * Errors: EINVAL (null / count < 0 / misaligned), ENOTONCURVE (pk not on the
+ *   curve or not reduced), ECUDA.  Async.                                   */
 PCMM_API int pcmm_encrypt(const uint8_t pk_h[64], const int32_t *b_d, const uint8_t *r_d, int64_t count, uint8_t *ct_d,
                  void *stream);
 

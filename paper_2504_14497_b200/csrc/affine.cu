@@ -145,7 +145,7 @@ __device__ __forceinline__ void aff_fetch(AffEnt &a, const uint32_t *__restrict_
     a.pre = fe{{p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w}};
     if (kind == kAffXyzz) {
         a.zz3 = fe{{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w}};
-        a.ok = !fe_is_zero(a.zz3);
+        a.ok = !fe_is_zero(a.zz3) && (q1.w & q1.z) != 0xffffffffu;   // not the pass-1 identity marker
     } else {
         a.ok = !fe_is_zero(a.Z);
     }
@@ -193,10 +193,14 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
         const AffIn a0 = kd == kAffProj ? aff_load_z(tab, e, entries) : aff_load_zzz(atab, e);
         if (kd == kAffProj) {
             aff_pass1_store(atab, e, entries, a0, acc);
-        } else if (a0.ok) {                                            // ZZZ = 0 stays for pass 2
+        } else if (a0.ok) {
             uint4 *dst = reinterpret_cast<uint4 *>(atab + e * kAffWords);
             dst[2] = make_uint4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
             dst[3] = make_uint4(acc.v[4], acc.v[5], acc.v[6], acc.v[7]);
+        } else {
+            // ZZZ = 0 (an identity ciphertext component): the identity marker is final here, so a
+            // CTA with nothing to invert can return before pass 2 (pass 2 sees the marker, aff_fetch)
+            st_aff_inf(atab + e * kAffWords);
         }
         if (a0.ok) {
             fe_mul(acc, acc, a0.z);

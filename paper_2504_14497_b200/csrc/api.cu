@@ -2,7 +2,8 @@
 // Host code only: argument validation, workspace carving, launch ordering on
 // the caller's stream, status reporting.  Every step of the PC-MM path runs in
 // the kernels of kernels.cu; nothing here computes on the host except keygen's
-// SplitMix64 draw of the secret scalar (R12).
+// SplitMix64 draw of the secret scalar (R12) and pcmm_encrypt's
+// on-curve check of the public key (argument validation).
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -190,6 +191,90 @@ bool in_range_1_qm1(const uint64_t w[4]) {   // 1 <= w <= q - 1, w big-endian wo
     return false;                              // == q
 }
 
+// ---- host-side public-key check for pcmm_encrypt (argument validation only; the
+// encryption itself runs on the device).  Plain 4 x 64-bit little-endian limbs,
+// 512-bit products reduced mod p by shift-and-subtract: slow and obviously right.
+typedef unsigned __int128 u128;
+const uint64_t kP[4] = {0xffffffffffffffffULL, 0x00000000ffffffffULL, 0x0000000000000000ULL,
+                        0xffffffff00000001ULL};       // p = 2^256 - 2^224 + 2^192 + 2^96 - 1 (little-endian limbs)
+const uint64_t kB[4] = {0x3bce3c3e27d2604bULL, 0x651d06b0cc53b0f6ULL, 0xb3ebbd55769886bcULL,
+                        0x5ac635d8aa3a93e7ULL};       // curve coefficient b (SEC 2)
+
+int cmp4(const uint64_t *a, const uint64_t *b) {
+    for (int i = 3; i >= 0; i--) {
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    }
+    return 0;
+}
+
+void sub4(uint64_t *a, const uint64_t *b) {   // a -= b (a >= b)
+    uint64_t br = 0;
+    for (int i = 0; i < 4; i++) {
+        const u128 d = (u128)a[i] - b[i] - br;
+        a[i] = (uint64_t)d;
+        br = (uint64_t)(d >> 64) & 1;
+    }
+}
+
+void mulmod4(uint64_t *r, const uint64_t *a, const uint64_t *b) {   // r = a b mod p (a, b < p)
+    uint64_t t[8] = {0};
+    for (int i = 0; i < 4; i++) {
+        uint64_t c = 0;
+        for (int j = 0; j < 4; j++) {
+            const u128 s = (u128)a[i] * b[j] + t[i + j] + c;
+            t[i + j] = (uint64_t)s;
+            c = (uint64_t)(s >> 64);
+        }
+        t[i + 4] = c;
+    }
+    uint64_t acc[4] = {0, 0, 0, 0};             // Horner over the 512 bits, msb first: acc = 2 acc + bit
+    for (int bit = 511; bit >= 0; bit--) {
+        const uint64_t top = acc[3] >> 63;
+        for (int i = 3; i > 0; i--) acc[i] = (acc[i] << 1) | (acc[i - 1] >> 63);
+        acc[0] = (acc[0] << 1) | ((t[bit >> 6] >> (bit & 63)) & 1);
+        if (top || cmp4(acc, kP) >= 0) sub4(acc, kP);   // 2 acc + 1 < 2p: one subtraction (mod 2^256 if top)
+    }
+    for (int i = 0; i < 4; i++) r[i] = acc[i];
+}
+
+void addmod4(uint64_t *r, const uint64_t *a, const uint64_t *b) {
+    uint64_t c = 0;
+    uint64_t s[4];
+    for (int i = 0; i < 4; i++) {
+        const u128 x = (u128)a[i] + b[i] + c;
+        s[i] = (uint64_t)x;
+        c = (uint64_t)(x >> 64);
+    }
+    if (c || cmp4(s, kP) >= 0) sub4(s, kP);
+    for (int i = 0; i < 4; i++) r[i] = s[i];
+}
+
+// canonical 64-byte point (x || y, big-endian) on P-256: x, y < p and y^2 = x^3 - 3x + b
+bool pk_on_curve_host(const uint8_t pk[64]) {
+    uint64_t x[4] = {0}, y[4] = {0};
+    for (int i = 0; i < 32; i++) {
+        x[3 - i / 8] = (x[3 - i / 8] << 8) | pk[i];
+        y[3 - i / 8] = (y[3 - i / 8] << 8) | pk[32 + i];
+    }
+    if (cmp4(x, kP) >= 0 || cmp4(y, kP) >= 0) return false;
+    uint64_t lhs[4], rhs[4], x3[4], neg3x[4], three_x[4];
+    mulmod4(lhs, y, y);
+    mulmod4(x3, x, x);
+    mulmod4(x3, x3, x);
+    addmod4(three_x, x, x);
+    addmod4(three_x, three_x, x);
+    uint64_t zero[4] = {0, 0, 0, 0};
+    if (cmp4(three_x, zero) == 0) {
+        for (int i = 0; i < 4; i++) neg3x[i] = 0;
+    } else {
+        for (int i = 0; i < 4; i++) neg3x[i] = kP[i];
+        sub4(neg3x, three_x);                    // p - 3x
+    }
+    addmod4(rhs, x3, neg3x);
+    addmod4(rhs, rhs, kB);
+    return cmp4(lhs, rhs) == 0;
+}
+
 }  // namespace
 
 namespace pcmm {
@@ -269,6 +354,10 @@ int pcmm_encrypt(const uint8_t pk_h[64], const int32_t *b_d, const uint8_t *r_d,
     bool zero = true;
     for (int i = 0; i < 64; i++) zero = zero && pk_h[i] == 0;
     if (zero) return fail(PCMM_ENOTONCURVE, "public key is the point at infinity");
+    if (!pk_on_curve_host(pk_h))
+        return fail(PCMM_ENOTONCURVE, "public key is not a point of P-256 (or a coordinate is not reduced)");
+    if (((uintptr_t)r_d & 15) || ((uintptr_t)ct_d & 15))
+        return fail(PCMM_EINVAL, "misaligned buffer (r / ct 16 B)");
     cudaStream_t s = (cudaStream_t)stream;
     LAUNCH("encrypt", s, launch_encrypt(pk_h, b_d, r_d, count, ct_d, s));
     return PCMM_OK;
@@ -462,6 +551,7 @@ int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t coun
         return fail(PCMM_EINVAL, "range too large (hi - lo < 2^26, |lo|, |hi| < 2^30)");
     if (count == 0) return PCMM_OK;
     if (!sk_h || !ct_d || !m_d || !status_d) return fail(PCMM_EINVAL, "null pointer");
+    if ((uintptr_t)ct_d & 15) return fail(PCMM_EINVAL, "misaligned buffer (ct 16 B)");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t tc = hi - lo + 1;
     uint32_t x[8];

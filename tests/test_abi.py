@@ -99,3 +99,34 @@ def test_validation_of_the_next_entry_points_without_gpu():
     assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 4, even, 512, p, p, p, 0, None) == P.PCMM_EINVAL
     assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 4, words, 4096, p, p, p, 0, None) == P.PCMM_ENOTSUP
     assert L.pcmm_paillier_mul(1, p, 4, 4, 4, 4, 5, words, 512, p, p, p, 0, None) == P.PCMM_ENOTSUP
+
+
+def test_encrypt_rejects_bad_public_keys_without_gpu():
+    # pcmm_encrypt validates H on the host (y^2 = x^3 - 3x + b, coordinates < p) before any launch;
+    # the expected verdicts come from tests/ecref.py (OpenSSL points, SEC 2 constants), not the library
+    from paper_2504_14497_b200 import pcmm as P
+    from tests import ecref
+    L = P.load()
+    p = ctypes.c_void_p(1 << 20)                       # aligned, never dereferenced: validation fails first
+    good = ecref.mulG(123456789)
+
+    def rc(pk, r=p, ct=p):
+        buf = ctypes.create_string_buffer(bytes(pk), 64)
+        return L.pcmm_encrypt(buf, p, r, 4, ct, None)
+
+    bad_y = bytearray(good)
+    bad_y[63] ^= 1                                     # off the curve
+    assert rc(bad_y) == P.PCMM_ENOTONCURVE
+    x = int.from_bytes(good[:32], "big")
+    y = int.from_bytes(good[32:], "big")
+    unreduced = x.to_bytes(32, "big") + (y + ecref.P).to_bytes(33, "big")[1:] if y + ecref.P < 2**256 else None
+    if unreduced is not None:                          # y + p as a 256-bit value: same residue, not reduced
+        assert rc(unreduced) == P.PCMM_ENOTONCURVE
+    assert rc(bytes(64)) == P.PCMM_ENOTONCURVE         # the identity
+    neg = x.to_bytes(32, "big") + (ecref.P - y).to_bytes(32, "big")    # -H is a valid key
+    assert rc(neg, r=ctypes.c_void_p((1 << 20) + 4)) == P.PCMM_EINVAL  # passes the curve check, misaligned r
+    assert rc(good, ct=ctypes.c_void_p((1 << 20) + 8)) == P.PCMM_EINVAL
+    for k in (1, 2, 3, ecref.Q - 1, 2**200 + 7):       # on-curve keys reach the alignment check only
+        assert rc(ecref.mulG(k), r=ctypes.c_void_p((1 << 20) + 1)) == P.PCMM_EINVAL
+    # x with y^2 = x^3 - 3x + b having no root: shift x until off-curve with y kept
+    assert rc((x ^ 1).to_bytes(32, "big") + good[32:]) == P.PCMM_ENOTONCURVE

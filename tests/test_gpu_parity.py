@@ -7,10 +7,13 @@ applied to the seeded synthetic inputs of `synth`; never from the CUDA path.
 
 * small configs (tiny, 64^3, ragged shapes): every output, oracle-encrypted inputs;
 * full BASELINE sizes (256^3, 512^3, ML): the launch configuration bench.py uses,
-  inputs encrypted on the GPU (that encryption is itself checked on a sample
-  against the oracle), outputs checked on a sample against the Eq. 5 closed form
-  evaluated by the oracle from (x, A, B, r) alone.
+  EVERY output compared byte for byte with the oracle's Cussen PC-MM (Alg. 3,
+  P:430-449) on oracle-encrypted inputs (the oracle, all host cores, ~1 min in
+  total on a 16-core box), the GPU encryption of the same (B, r) compared with
+  the oracle's over all n*l ciphertexts, and a sample of outputs checked a second,
+  independent way against the Eq. 5 closed form evaluated from (x, A, B, r) alone.
 """
+import functools
 import random
 
 import numpy as np
@@ -298,6 +301,40 @@ def test_accumulator_exceptional_cases(w):
     assert (exp[3 * l:4 * l] == 0).all()            # row 3 sums to the identity in every column
 
 
+def test_all_identity_ciphertexts_consecutive_tables():
+    # Every ciphertext is (inf, inf) (64 + 64 zero bytes are valid input) in a launch that takes
+    # k_tables_fast (unsigned, consecutive columns, 2 n l >= 65536): every table entry is the identity,
+    # so no CTA of k_affine has anything to invert, and every output must be (inf, inf)
+    m, n, l = 8, 256, 128
+    cfg = synth.Config("allinf", m, n, l, 4, False, 0, 255, 4242)
+    I = synth.make_instance(cfg)
+    A = I.A.copy()
+    A[:, :] = (np.arange(m)[:, None] % 15) + 1          # every column consecutive {1..8}
+    ct = np.zeros((n * l, 128), dtype=np.uint8)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, A, ct, l, 4)
+    assert (exp == 0).all()
+    assert (_gpu_pcmm(A, ct, l, 4, False, P.CUSSEN) == 0).all()
+    # and half of the columns identity, half not: mixed CTAs
+    x = synth.keygen_secret(cfg.seed)
+    ct2 = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct2[: n // 2] = 0
+    ct2 = np.ascontiguousarray(ct2.reshape(n * l, 128))
+    exp2, _ = oracle.pcmm(oracle.CUSSEN, A, ct2, l, 4)
+    assert (_gpu_pcmm(A, ct2, l, 4, False, P.CUSSEN) == exp2).all()
+
+
+def test_encrypt_rejects_off_curve_key():
+    sk, pk = P.keygen(3)
+    bad = bytearray(pk)
+    bad[40] ^= 4
+    b = torch.zeros(4, dtype=torch.int32, device="cuda")
+    r = torch.ones((4, 32), dtype=torch.uint8, device="cuda")
+    with pytest.raises(P.PCMMError) as e:
+        P.encrypt(bytes(bad), b, r)
+    assert e.value.code == P.PCMM_ENOTONCURVE
+    assert P.encrypt(pk, b, r).shape == (4, 128)
+
+
 def test_error_reporting():
     I = synth.make_instance(synth.CONFIGS["c64"], m=8, n=8, l=8, seed=3)
     x = synth.keygen_secret(3)
@@ -342,13 +379,57 @@ def _full_size(name, path, samples):
     return out
 
 
+@functools.lru_cache(maxsize=None)
+def _oracle_full(name):
+    """The oracle's answer for a BASELINE config: (instance, pk, Enc(B), C) with Enc(B) from
+    oracle.encrypt and C = oracle.pcmm(CUSSEN) (Alg. 3 step by step, all host cores)."""
+    cfg = synth.CONFIGS[name]
+    I = synth.make_instance(cfg)
+    pk = oracle.pubkey(I.x)
+    ct = oracle.encrypt(pk, I.B.reshape(-1), I.r_be)
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, cfg.l, cfg.w)
+    return I, pk, ct, exp
+
+
+def _every_output(name, path):
+    cfg = synth.CONFIGS[name]
+    I, pk, ct, exp = _oracle_full(name)
+    out = P.pcmm(cuda(I.A), cuda(ct), cfg.l, cfg.w, cfg.signed, path=path).cpu().numpy()
+    bad = np.nonzero((out != exp).any(axis=1))[0]
+    assert bad.size == 0, (name, path, bad.size, [(int(e) // cfg.l, int(e) % cfg.l) for e in bad[:8]])
+    return I, out
+
+
 @pytest.mark.parametrize("name", ["c256", "c512", "ml"])
-def test_full_size_cussen_sampled(name):
-    _full_size(name, P.CUSSEN, 40)
+def test_full_size_cussen_every_output(name):
+    # north_star: bit-exact agreement with the CPU oracle on every BASELINE config (P:424: Cussen
+    # "always performs exact reconstruction"); every one of the m*l outputs, launch configuration of bench.py
+    cfg = synth.CONFIGS[name]
+    I, out = _every_output(name, P.CUSSEN)
+    # second, independent check of a sample: the Eq. 5 closed form from (x, A, B, r) alone
+    r = I.r_be.reshape(cfg.n, cfg.l, 32)
+    g = np.random.default_rng(cfg.seed)
+    for (i, j) in [(0, 0), (cfg.m - 1, cfg.l - 1)] + [(int(g.integers(cfg.m)), int(g.integers(cfg.l)))
+                                                      for _ in range(6)]:
+        assert out[i * cfg.l + j].tobytes() == oracle.closed_form(I.x, I.A[i], I.B[:, j], r[:, j]), (name, i, j)
 
 
-def test_full_size_c256_schoolbook_sampled():
-    _full_size("c256", P.SCHOOLBOOK, 16)
+def test_full_size_c256_schoolbook_every_output():
+    # the comparison path (P:227-233) on the headline config, every output
+    _every_output("c256", P.SCHOOLBOOK)
+
+
+@pytest.mark.parametrize("name", ["c256", "c512", "ml"])
+def test_full_size_gpu_encryption_every_ciphertext(name):
+    # pcmm_encrypt (P:180) on the full B of each config equals the oracle's Encrypt for every ciphertext
+    I, pk, ct, _ = _oracle_full(name)
+    got = P.encrypt(pk, cuda(I.B.reshape(-1).astype(np.int32)), cuda(I.r_be)).cpu().numpy()
+    assert (got == ct).all()
+
+
+def test_full_size_gpu_encrypted_inputs_sampled():
+    # the bench's own input path (B encrypted on the GPU) at 256^3, sampled vs Eq. 5
+    _full_size("c256", P.CUSSEN, 8)
 
 
 @pytest.mark.parametrize("name,path", [("c512", "schoolbook"), ("ml", "schoolbook"), ("c256", "strassen"),
