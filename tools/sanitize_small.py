@@ -5,7 +5,7 @@ Covers, on shapes that take each launch path (api.cu / kernels.cu dispatch):
   k_tables_x (2^w >= 128 slots), k_tables_scan (few long tables), k_accum<S> for S = 4, 8, 16
   (shared-memory staging, several k-chunks, split-k) + k_reduce, k_accum_g (w > 4),
   k_normalize, k_school, the wide path (k_plan_wide, k_tables_wide, k_tables_wide_scan,
-  k_accum_gw), Strassen, comb encryption, BSGS and table decryption.
+  k_accum_gw), Strassen, comb encryption, BSGS and table decryption, Paillier (warp and per-thread).
 Every run is also checked Cussen == schoolbook (bytes), so a silent corruption fails here too.
 
   compute-sanitizer --tool memcheck python tools/sanitize_small.py
@@ -70,5 +70,19 @@ for c in cases:
         mb, sb = P.decrypt_bsgs(sk, bctx, 8, e1, -1000, 1000)
         assert int(sb.abs().sum()) == 0 and torch.equal(mb.cpu(), b.cpu().long())
         print("next2 ok", flush=True)
+if not only or "paillier" in only:
+    # NEXT-4: warp-cooperative (3072-bit) and per-thread (1024-bit, PCMM_PAILLIER_WARP=0 in the env) kernels;
+    # random units as ciphertexts (the arithmetic does not depend on what they encrypt); Cussen == schoolbook
+    for nbits, (m, nn, l), w in ((3072, (4, 6, 3), 4), (1024, (6, 10, 3), 8)):
+        p_, q_ = synth.paillier_primes(nbits, nbits // 2)
+        n = p_ * q_
+        gen = synth.SplitMix64(nbits + w)
+        A = torch.from_numpy(gen.small(0, (1 << w) - 1, m * nn).reshape(m, nn).astype(np.uint8)).cuda()
+        R = synth.paillier_random_units(nbits, n, nn * l)
+        ct = P.to_words([x * x % (n * n) for x in R], nbits // 32).cuda()
+        o1 = P.from_words(P.paillier_mul(P.CUSSEN, A, ct, l, w, n * n))
+        o2 = P.from_words(P.paillier_mul(P.SCHOOLBOOK, A, ct, l, w, n * n))
+        assert o1 == o2, nbits
+        print("paillier", nbits, "ok", flush=True)
 torch.cuda.synchronize()
 print("all ok")
