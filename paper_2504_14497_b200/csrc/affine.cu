@@ -56,58 +56,6 @@ __device__ __forceinline__ void aff_pass1_store(uint32_t *__restrict__ atab, int
     }
 }
 
-// One inversion per CTA (128 lanes x `batch` entries): lane products -> warp
-// prefix/suffix products (shuffles) -> the four warp totals -> lane 0 of warp 0
-// inverts their product and hands each warp the inverse of its total; each lane
-// then recovers 1 / (its product) = inv(warp total) x (prefix before it) x
-// (suffix after it).  The other warps wait at the barrier while other CTAs run.
-// kFermat: the CTA's one inversion by Fermat's chain (fewer registers: 3+ CTAs per
-// SM keep the two passes busy on large tables) or by divsteps (4x shorter latency:
-// small tables, where that one inversion is the kernel's critical path)
-template <bool kFermat>
-__device__ __forceinline__ fe cta_inverse(const fe &acc, fe *wtot, fe *winv) {
-    const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
-    fe one;
-    fe_one_mont(one);
-    // warp-inclusive prefix (Q) and suffix (S) products of the lane products
-    fe Q = acc, S = acc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const fe q = fe_shfl_up(Q, d), sv = fe_shfl_down(S, d);
-        fe qm, sm;
-        fe_mul(qm, Q, q);
-        fe_mul(sm, S, sv);
-        if (lane >= d) Q = qm;
-        if (lane + d < 32) S = sm;
-    }
-    if (lane == 31) wtot[warp] = Q;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        fe p1 = wtot[0], p2, p3, tot, s2, s1, inv, x;
-        fe_mul(p2, p1, wtot[1]);
-        fe_mul(p3, p2, wtot[2]);
-        fe_mul(tot, p3, wtot[3]);
-        fe_mul(s2, wtot[2], wtot[3]);
-        fe_mul(s1, wtot[1], s2);
-        if (kFermat) fe_inv_fermat(inv, tot);
-        else fe_inv(inv, tot);
-        fe_mul(winv[0], inv, s1);                  // 1 / W0
-        fe_mul(x, inv, p1);
-        fe_mul(winv[1], x, s2);                    // 1 / W1
-        fe_mul(x, inv, p2);
-        fe_mul(winv[2], x, wtot[3]);               // 1 / W2
-        fe_mul(winv[3], inv, p3);                  // 1 / W3
-    }
-    __syncthreads();
-    fe qprev = fe_shfl_up(Q, 1), snext = fe_shfl_down(S, 1);
-    if (lane == 0) qprev = one;
-    if (lane == 31) snext = one;
-    fe inv;
-    fe_mul(inv, winv[warp], qprev);
-    fe_mul(inv, inv, snext);                       // 1 / acc (this lane's product)
-    return inv;
-}
-
 // Entry kinds for k_affine: homogeneous (X : Y : Z) from k_tables, or, in a
 // consecutive column (k_tables_fast), slots 2..n1 hold XYZZ (X, Y, ZZ in the
 // projective slot, ZZZ in the x half of the affine slot: 1/ZZZ from the batch,
@@ -158,8 +106,10 @@ template <bool kFermat>
 __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t *__restrict__ tab, int64_t entries,
                                                                   int batch, uint32_t *__restrict__ atab,
                                                                   const ColPlan *__restrict__ plans, int n, int l,
-                                                                  int S, int N, int fast) {
+                                                                  int S, int N, int fast,
+                                                                  const int *__restrict__ general) {
     __shared__ fe wtot[4], winv[4];
+    if (fast == 2 && general != nullptr && *general == 0) return;     // every column done by k_tables_coz
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // entry e = ((c n + k) l + j) S + slot, S a power of two; plans != nullptr only on the byte path;
@@ -172,8 +122,10 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
         const uint32_t e32 = (uint32_t)e;
         const ColPlan &pl = plans[small ? (e32 / sl) % (uint32_t)n : (int)((e / ((int64_t)S * l)) % n)];
         const int slot = (int)(e & (int64_t)(S - 1));
-        if (fast && col_consecutive(pl, N))
+        if (fast && col_consecutive(pl, N)) {
+            if (fast == 2) return kAffSkip;                                // k_tables_aff: final already
             return (slot >= 2 && slot <= pl.n[0]) ? (PCMM_TFAST_PROJ ? kAffProj : kAffXyzz) : kAffSkip;
+        }
         // k_tables leaves slot 0 and the unused slots unwritten: the identity marker is written here
         return (slot >= 1 && slot <= pl.n[0]) ? kAffProj : kAffInf;
     };
@@ -246,7 +198,7 @@ __global__ void __launch_bounds__(128, PCMM_AFFINE_MINB) k_affine(const uint32_t
 }
 
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
-                          const ColPlan *plans, int n, int l, int S, int N, int fast) {
+                          const ColPlan *plans, int n, int l, int S, int N, int fast, const int *general) {
     if (entries <= 0) return cudaSuccess;
     // up to 32 entries per lane (one inversion per 4096 entries), fewer when that
     // would leave fewer than ~4 warps per SM (256^3: batch 32 0.48 ms, 16 0.55, 8 0.76)
@@ -275,10 +227,10 @@ cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *ata
     // 256^3 0.309 vs 0.324 ms, 512^3 0.299 vs 0.314, ML 0.246 vs 0.261, 64^3 0.091 vs 0.107
     if (inv_env == 1)
         k_affine<true><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N,
-                                                                  fast);
+                                                                  fast, general);
     else
         k_affine<false><<<blocks_for(threads, 128), 128, 0, s>>>(tables, entries, batch, atables, plans, n, l, S, N,
-                                                                   fast);
+                                                                   fast, general);
     return cudaGetLastError();
 }
 

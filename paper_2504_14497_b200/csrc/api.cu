@@ -381,7 +381,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     int *status = (int *)ws;
     uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
     uint32_t *out = (uint32_t *)ctC_proj_d;
-    CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
+    CK(cudaMemsetAsync(status, 0, 8, s), "memset status");      // [0] error bits, [1] k_plan's general-column flag
     LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
     if (path == PCMM_PATH_SCHOOLBOOK) {
         LAUNCH("schoolbook", s, launch_schoolbook(A_d, m, n, l, w, is_signed, bsoa, out, status, s));
@@ -393,15 +393,21 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
     // consecutive-column tables (k_tables_fast): unsigned A, launches that fill the GPU
     // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
-    const int fast = tables_fast_on() && !is_signed && 2LL * n * l >= 65536;
+    // (k_tables_coz, default: the same columns, tables and affine conversion in one kernel; k_affine skips them)
+    const int amode = tables_coz_mode();
+    const int aff = !is_signed && iters >= 2 && (amode == 2 || (amode == 1 && 2LL * n * l >= 65536));
+    const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * n * l >= 65536);
     LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, is_signed, tables,
-                                            (uint32_t *)(ws + L.scratch), s, fast, std::min(m, L.slots - 1)));
+                                            (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1)));
     uint32_t *atables = (uint32_t *)(ws + L.scratch);
-    if (fast) {
-        // after k_tables: the affine tables share the region of k_tables' upper-level scratch
+    // after k_tables: the affine tables share the region of k_tables' upper-level scratch
+    if (fast == 2) {
+        LAUNCH("tables_coz", s, launch_tables_coz(bsoa, plans, n, l, iters, L.slots, tables, atables, s));
+    } else if (fast) {
         LAUNCH("tables_fast", s, launch_tables_fast(bsoa, plans, n, l, iters, L.slots, tables, atables, s));
     }
-    LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s, plans, n, l, L.slots, iters, fast));
+    LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s, plans, n, l, L.slots, iters, fast,
+                                      status + 1));
     const int64_t cnt = (int64_t)m * l;
     uint32_t *acc_out = L.ksplit == 1 ? out : (uint32_t *)(ws + L.partial);
     const int64_t split_stride = L.ksplit == 1 ? 0 : 2LL * kPtWords * cnt;
@@ -487,7 +493,7 @@ static int mul_wide(int path, const int32_t *A_d, int m, int n, int l, int w, in
     int *status = (int *)ws;
     uint32_t *bsoa = (uint32_t *)(ws + L.bsoa);
     uint32_t *out = (uint32_t *)ctC_proj_d;
-    CK(cudaMemsetAsync(status, 0, 4, s), "memset status");
+    CK(cudaMemsetAsync(status, 0, 8, s), "memset status");      // [0] error bits, [1] k_plan's general-column flag
     LAUNCH("import", s, launch_import(ctB_d, (int64_t)n * l, bsoa, status, s));
     if (path == PCMM_PATH_SCHOOLBOOK) {
         LAUNCH("schoolbook", s, launch_schoolbook_wide(A_d, m, n, l, w, is_signed, bsoa, out, status, s));

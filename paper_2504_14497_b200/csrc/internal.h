@@ -46,13 +46,21 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
 // plans != nullptr: entries of consecutive columns (built by k_tables_fast) are skipped
 // plans != nullptr (byte path): per-column entry kinds (slot 0 / unused slots -> identity markers without
 // reading the tables; fast != 0: consecutive columns come from k_tables_fast)
+// general != nullptr with fast = 2: device flag written by k_plan (some column is not consecutive); 0 -> no work
 cudaError_t launch_affine(const uint32_t *tables, int64_t entries, uint32_t *atables, cudaStream_t s,
-                          const ColPlan *plans = nullptr, int n = 0, int l = 0, int S = 0, int N = 0, int fast = 0);
+                          const ColPlan *plans = nullptr, int n = 0, int l = 0, int S = 0, int N = 0, int fast = 0,
+                          const int *general = nullptr);
 // consecutive columns (s^(1) = {1..n1}): XYZZ prefix sums + fused affine conversion
 // (k_tables_fast); k_tables skips them when tables_fast_on()
 int tables_fast_on();
 cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
                                uint32_t *tables, uint32_t *atables, cudaStream_t s);
+// consecutive columns, tables and affine conversion in one kernel (taff.cu k_tables_coz: co-Z
+// prefix chain, one CTA-shared inversion); k_affine then skips those columns (fast = 2).
+// tables: the projective table region (per-entry X, Y, lambda parked there)
+cudaError_t launch_tables_coz(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
+                              uint32_t *tables, uint32_t *atables, cudaStream_t s);
+int tables_coz_mode();   // PCMM_TABLES_COZ: 0 off, 1 auto (default), 2 always (unsigned A)
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
 // kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
 inline int max_upper(int w) { return w <= 4 ? 8 : 32; }

@@ -112,6 +112,8 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
             for (int e = 0; e < ns; e++) P->sN[e] = s[e];
         }
     }
+    // status[1]: some column is not consecutive (k_tables / k_affine have work beside k_tables_coz)
+    if (!col_consecutive(*P, N)) atomicOr(status + 1, 1);
 }
 
 // ------------------------------------------------------------ a2 + a3: tables
@@ -956,6 +958,15 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
 }
 
 int tables_fast_on() { return tables_fast_enabled(); }
+
+int tables_coz_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PCMM_TABLES_COZ");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
 
 cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
                                uint32_t *tables, uint32_t *atables, cudaStream_t s) {

@@ -224,13 +224,15 @@ def test_degenerate_matrices():
     assert (_gpu_pcmm(I.A, ct2, 8, 4, False, P.CUSSEN) == exp).all()
 
 
-@pytest.mark.parametrize("w", [2, 4])
-def test_consecutive_column_tables_mixed(w):
-    # A launch large enough for k_tables_fast (2 n l >= 65536): columns whose level-1
-    # set is {1..n1} (built by XYZZ prefix sums, converted by k_affine's XYZZ branch)
-    # next to columns that are not (k_tables + homogeneous k_affine), an all-zero
-    # column, and identity ciphertexts in a consecutive column.
-    m, n, l = 8, 256, 128
+@pytest.mark.parametrize("w,l", [(2, 128), (4, 128), (4, 130)])
+def test_consecutive_column_tables_mixed(w, l):
+    # A launch large enough for the consecutive-column kernels (2 n l >= 65536): columns whose
+    # level-1 set is {1..n1} (k_tables_coz by default: co-Z prefix chain converted to affine in the
+    # same kernel; PCMM_TABLES_COZ=0: XYZZ prefix sums converted by k_affine's XYZZ branch) next to
+    # columns that are not (k_tables + homogeneous k_affine), an all-zero column, identity
+    # ciphertexts in a consecutive column, n1 = 1, 5, 7 (not powers of two), and l = 130 so that
+    # warps straddle columns k with different n1.
+    m, n = 8, 256
     cfg = synth.Config("mixed", m, n, l, w, False, 0, 255, 77 + w)
     I = synth.make_instance(cfg)
     A = I.A.copy()
@@ -240,6 +242,9 @@ def test_consecutive_column_tables_mixed(w):
     A[:, 2] = 0                                          # empty column
     A[:, 3] = [1, 3] * (m // 2)                          # {1, 3}: not consecutive
     A[:, 4] = [1, 2] * (m // 2)                          # consecutive, n1 = 2
+    A[:, 5] = 1                                          # consecutive, n1 = 1 (no rounds)
+    A[:, 6] = [(i % 5) + 1 for i in range(m)] if w > 2 else 3 - (np.arange(m) % 3)   # n1 = 5 (w = 2: 3)
+    A[:, 7] = [(i % 7) + 1 for i in range(m)] if w > 2 else 1 + (np.arange(m) % 2)   # n1 = 7 (w = 2: 2)
     x = synth.keygen_secret(cfg.seed)
     ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
     ct[0, 5] = 0                                         # (inf, inf) in consecutive column k = 0
@@ -726,6 +731,22 @@ def test_wide_block_scan_forced():
     env = dict(os.environ, PCMM_WIDE_SCAN="2")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__,
                         "-k", "test_wide_every_output or test_wide_chunked"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_consecutive_table_kernels_forced(mode):
+    # PCMM_TABLES_COZ=0: the XYZZ consecutive-column kernel (k_tables_fast + k_affine's XYZZ branch);
+    # 2: the fused co-Z kernel (k_tables_coz) for every unsigned launch, also the small ones
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_TABLES_COZ=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or "
+                        "test_consecutive_column or test_all_identity or test_vector_times"],
+                       env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
