@@ -559,6 +559,15 @@ __device__ PCMM_HOTCALL fe4 fe_sqr_mul3_hot(const fe c, const fe a0, const fe b0
     return r;
 }
 
+// (c^2, a0 b0, a1 b1): the XYZZ doubling's third group (jac.cuh xyzz_dbl)
+__device__ PCMM_HOTCALL fe3 fe_sqr_mul2_hot(const fe c, const fe a0, const fe b0, const fe a1, const fe b1) {
+    fe3 r;
+    fe_sqr_fast(r.x, c);
+    fe_mul_fast(r.y, a0, b0);
+    fe_mul_fast(r.z, a1, b1);
+    return r;
+}
+
 __device__ PCMM_HOTCALL fe4 fe_mul4_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
                                         const fe b2, const fe a3, const fe b3) {
     fe4 r;

@@ -72,6 +72,9 @@ cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int
 cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);
 cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
                               uint32_t *out, int *status, cudaStream_t s);
+// the XYZZ schoolbook (school.cu k_school_xyzz), launch_schoolbook with PCMM_SCHOOL_XYZZ=1
+cudaError_t launch_schoolbook_xyzz(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
+                                   uint32_t *out, int *status, cudaStream_t s);
 cudaError_t launch_normalize(const uint32_t *proj, int64_t count, uint8_t *ct, cudaStream_t s);
 cudaError_t launch_encrypt(const uint8_t *pk64, const int32_t *b, const uint8_t *r, int64_t count, uint8_t *ct,
                            cudaStream_t s);

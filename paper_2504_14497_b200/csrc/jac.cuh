@@ -205,6 +205,62 @@ __device__ __forceinline__ void xyzz_init(xyzz &A) {
     A.inf = 1;
 }
 
+// A = 2 (x, y) for an affine input (mdbl-2008-s-1, a = -3): U = 2y, V = U^2,
+// W = U V, S = x V, M = 3 (x^2 - 1), X3 = M^2 - 2S, Y3 = M (S - X3) - W y,
+// ZZ3 = V, ZZZ3 = W: 4M + 3S.  y != 0 on P-256 (no point of order 2).
+__device__ __forceinline__ void xyzz_dbl_aff(xyzz &A, const fe &x, const fe &y) {
+    fe U, V, W, Sv, M, x2, t, X3, D;
+    fe_add(U, y, y);                               // U = 2y
+    fe_sqr(V, U);                                  // V = U^2
+    fe_mul(W, U, V);                               // W = U V
+    fe_mul(Sv, x, V);                              // S = x V
+    fe_sqr(x2, x);
+    fe one;
+    fe_one_mont(one);
+    fe_sub(t, x2, one);
+    fe_add(M, t, t);
+    fe_add(M, M, t);                               // M = 3 (x^2 - 1) = 3 x^2 + a, a = -3
+    fe_sqr(X3, M);
+    fe_sub(X3, X3, Sv);
+    fe_sub(X3, X3, Sv);                            // X3 = M^2 - 2S
+    fe_sub(D, Sv, X3);
+    fe_mul(D, M, D);
+    fe_mul(t, W, y);
+    fe_sub(A.Y, D, t);                             // Y3 = M (S - X3) - W y
+    A.X = X3;
+    A.ZZ = V;
+    A.ZZZ = W;
+    A.inf = 0;
+}
+
+// A <- 2A in XYZZ (dbl-2008-s-1, a = -3): U = 2Y, V = U^2, W = U V, S = X V,
+// M = 3 (X - ZZ)(X + ZZ), X3 = M^2 - 2S, Y3 = M (S - X3) - W Y, ZZ3 = V ZZ,
+// ZZZ3 = W ZZZ: 7M + 2S.  The identity stays the identity.
+__device__ __forceinline__ void xyzz_dbl(xyzz &A) {
+#ifdef __CUDA_ARCH__
+    if (A.inf) return;
+    fe U, V, t0, t1, M, X3, D;
+    fe_add(U, A.Y, A.Y);
+    fe_sqr(V, U);
+    fe_sub(t0, A.X, A.ZZ);
+    fe_add(t1, A.X, A.ZZ);
+    const fe4 g = fe_mul4_hot(U, V, A.X, V, t0, t1, V, A.ZZ);    // W, S, (X - ZZ)(X + ZZ), ZZ3
+    const fe &W = g.x, &Sv = g.y;
+    fe_add(M, g.z, g.z);
+    fe_add(M, M, g.z);                                            // M = 3 (X - ZZ)(X + ZZ)
+    const fe3 h = fe_sqr_mul2_hot(M, W, A.Y, W, A.ZZZ);          // M^2, W Y, ZZZ3
+    fe_sub(X3, h.x, Sv);
+    fe_sub(X3, X3, Sv);                                           // X3 = M^2 - 2S
+    fe_sub(D, Sv, X3);
+    fe MD;
+    fe_mul(MD, M, D);                                             // M (S - X3)
+    fe_sub(A.Y, MD, h.y);                                         // Y3 = M (S - X3) - W Y
+    A.X = X3;
+    A.ZZ = g.w;
+    A.ZZZ = h.z;
+#endif
+}
+
 // homogeneous (X : Y : Z), Z != 0  ->  XYZZ (X Z, Y Z^2, Z^2, Z^3)
 __device__ __forceinline__ void xyzz_from_proj(xyzz &A, const pt &o) {
 #ifdef __CUDA_ARCH__

@@ -374,30 +374,6 @@ __global__ void __launch_bounds__(kTScanT) k_tables_scan(const uint32_t *__restr
 // jac.cuh) instead of a complete projective addition (12M + 2m_b), and T[2] = 2P
 // an affine-input doubling (4M + 3S).  The XYZZ entries go to k_affine (6M + 1S
 // per entry there, against 5M for a homogeneous one).  Other columns: k_tables.
-__device__ __forceinline__ void xyzz_dbl_aff(xyzz &A, const fe &x, const fe &y) {
-    fe U, V, W, Sv, M, x2, t, X3, D;
-    fe_add(U, y, y);                               // U = 2y
-    fe_sqr(V, U);                                  // V = U^2
-    fe_mul(W, U, V);                               // W = U V
-    fe_mul(Sv, x, V);                              // S = x V
-    fe_sqr(x2, x);
-    fe one;
-    fe_one_mont(one);
-    fe_sub(t, x2, one);
-    fe_add(M, t, t);
-    fe_add(M, M, t);                               // M = 3 (x^2 - 1) = 3 x^2 + a, a = -3
-    fe_sqr(X3, M);
-    fe_sub(X3, X3, Sv);
-    fe_sub(X3, X3, Sv);                            // X3 = M^2 - 2S
-    fe_sub(D, Sv, X3);
-    fe_mul(D, M, D);
-    fe_mul(t, W, y);
-    fe_sub(A.Y, D, t);                             // Y3 = M (S - X3) - W y
-    A.X = X3;
-    A.ZZ = V;
-    A.ZZZ = W;
-    A.inf = 0;
-}
 
 __device__ __forceinline__ void st_fe2(uint32_t *d, const fe &a, const fe &b) {
     uint4 *q = reinterpret_cast<uint4 *>(d);
@@ -642,8 +618,12 @@ __global__ void __launch_bounds__(128) k_school(const int8_t *__restrict__ A, in
                                                int is_signed, const uint32_t *__restrict__ bsoa,
                                                uint32_t *__restrict__ out, int *__restrict__ status) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int jb = blockIdx.x, c = blockIdx.z;
-    const int i = blockIdx.y * 4 + warp;
+    const int jblocks = (l + 31) / 32, rblocks = (m + 3) / 4;            // 1-D grid: (c, row block, j block)
+    int64_t bb = blockIdx.x;
+    const int jb = (int)(bb % jblocks);
+    bb /= jblocks;
+    const int c = (int)(bb / rblocks);
+    const int i = (int)(bb % rblocks) * 4 + warp;
     if (i >= m) return;
     const int j = jb * 32 + lane;
     const int jj = min(j, l - 1);
@@ -981,8 +961,15 @@ cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t co
 
 cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
                               uint32_t *out, int *status, cudaStream_t s) {
-    dim3 grid((unsigned)((l + 31) / 32), (unsigned)((m + 3) / 4), 2);
-    k_school<<<grid, 128, 0, s>>>(A, m, n, l, w, is_signed, bsoa, out, status);
+    // PCMM_SCHOOL_XYZZ=1: the XYZZ schoolbook (school.cu; fewer products, measured slower)
+    static int xz = -1;
+    if (xz < 0) {
+        const char *e = getenv("PCMM_SCHOOL_XYZZ");
+        xz = e ? atoi(e) : 0;
+    }
+    if (xz) return launch_schoolbook_xyzz(A, m, n, l, w, is_signed, bsoa, out, status, s);
+    const int64_t blocks = (int64_t)((l + 31) / 32) * ((m + 3) / 4) * 2;
+    k_school<<<(unsigned)blocks, 128, 0, s>>>(A, m, n, l, w, is_signed, bsoa, out, status);
     return cudaGetLastError();
 }
 

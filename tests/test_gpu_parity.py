@@ -751,6 +751,21 @@ def test_consecutive_table_kernels_forced(mode):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_xyzz_schoolbook_forced():
+    # the XYZZ schoolbook kernel (school.cu, PCMM_SCHOOL_XYZZ=1) on the every-output cases, including the
+    # exceptional accumulator cases (equal and opposite terms) and identity ciphertexts
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_SCHOOL_XYZZ="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or "
+                        "test_accumulator_exceptional or test_xyzz_level1 or test_extreme_values"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_byte_block_scan_forced():
     # the byte path's block-scan table kernel (k_tables_scan) forced on the every-output cases
     import os
