@@ -55,9 +55,56 @@ std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- workspace
 struct Layout {
-    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, scratch = 0, partial = 0, total = 0;
+    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, scratch = 0, partial = 0, bsoa_c = 0, total = 0;
     int rows = 128, ksplit = 1, slots = 16, maxup = 8;
+    int kc = 0;                            // inner indices per table chunk (= n: one chunk)
 };
+
+// split-k factor of k_accum for an (m, n, l) accumulation: minimise the quantised
+// wave count per unit of work, ceil(base*ks / resident) / ks, plus a small charge
+// per extra split (the k_reduce additions and per-CTA chunk overheads).
+static int choose_ksplit(int m, int n, int l, int w) {
+    const int rows = accum_rows();
+    const int rowblocks = (m + rows - 1) / rows;
+    const int64_t base = (int64_t)l * 2 * rowblocks;
+    const int slots = table_slots(w);
+    const double resident = (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(slots) : accum_global_ctas_per_sm());
+    // On the shared-memory path only splits whose k-range is a whole number of table chunks
+    // are considered when there are any besides 1 (measured: 256^3 2 splits 4.306 ms vs 3 ragged
+    // ones 4.323, 512^3 4 splits 24.50 vs 3: 24.88, ML 16 splits 2.88 vs 10: 2.92).
+    const int kch = w <= 4 ? accum_chunk(slots) : 0;
+    bool any_aligned = false;
+    for (int cand = 2; cand <= 16 && cand <= n && kch && n >= 4 * kch; cand++)   // (64^3: latency regime)
+        if (n % (cand * kch) == 0) any_aligned = true;
+    int ks = 1;
+    double best = 1e30;
+    for (int cand = 1; cand <= 16 && cand <= n; cand++) {
+        if (any_aligned && cand > 1 && n % (cand * kch) != 0) continue;
+        const double waves = std::ceil((double)base * cand / resident);
+        const double cost = waves / cand * (1.0 + 0.01 * (cand - 1)) + (n / cand < 8 ? 1.0 : 0.0);
+        if (cost < best - 1e-9) { best = cost; ks = cand; }
+    }
+    if (const char *e = getenv("PCMM_KSPLIT")) {         // measurement override (tools/)
+        const int v = atoi(e);
+        if (v >= 1 && v <= n) ks = v;
+    }
+    return ks;
+}
+
+// Table memory of the byte path (tables + k_tables scratch / affine tables) per inner index k;
+// above the budget (PCMM_BYTE_BUDGET_MB, default 2048) the Cussen path builds and consumes the
+// tables in chunks of kc inner indices (the imported rows of the chunk copied to their own
+// buffer, each chunk's accumulation added into the running output).
+static size_t byte_table_bytes_per_k(int l, int w) {
+    const size_t S = (size_t)table_slots(w), mu = (size_t)max_upper(w);
+    return 2 * (size_t)l * (S * kPtWords * 4 + std::max(2 * mu * kPtWords * 4, S * kAffWords * 4));
+}
+
+static size_t byte_budget() {
+    size_t budget = (size_t)2 << 30;
+    if (const char *e = getenv("PCMM_BYTE_BUDGET_MB")) budget = (size_t)atoll(e) << 20;
+    return budget;
+}
 
 Layout layout(int m, int n, int l, int w, int path) {
     Layout L;
@@ -67,48 +114,46 @@ Layout layout(int m, int n, int l, int w, int path) {
     off = align256(off + cnt * 2 * kPtWords * 4);
     if (path == PCMM_PATH_CUSSEN) {
         L.rows = accum_rows();
-        const int rowblocks = (m + L.rows - 1) / L.rows;
-        const int64_t base = (int64_t)l * 2 * rowblocks;
-        // split-k factor: minimise the quantised wave count per unit of work,
-        // ceil(base*ks / resident) / ks, plus a small charge per extra split
-        // (the k_reduce additions and per-CTA chunk overheads).
         L.slots = table_slots(w);
         L.maxup = max_upper(w);
-        const double resident =
-            (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(L.slots) : accum_global_ctas_per_sm());
-        // On the shared-memory path only splits whose k-range is a whole number of table chunks
-        // are considered when there are any besides 1 (measured: 256^3 2 splits 4.306 ms vs 3 ragged
-        // ones 4.323, 512^3 4 splits 24.50 vs 3: 24.88, ML 16 splits 2.88 vs 10: 2.92).
-        const int kch = w <= 4 ? accum_chunk(L.slots) : 0;
-        bool any_aligned = false;
-        for (int cand = 2; cand <= 16 && cand <= n && kch && n >= 4 * kch; cand++)   // (64^3: latency regime)
-            if (n % (cand * kch) == 0) any_aligned = true;
-        int ks = 1;
-        double best = 1e30;
-        for (int cand = 1; cand <= 16 && cand <= n; cand++) {
-            if (any_aligned && cand > 1 && n % (cand * kch) != 0) continue;
-            const double waves = std::ceil((double)base * cand / resident);
-            const double cost = waves / cand * (1.0 + 0.01 * (cand - 1)) + (n / cand < 8 ? 1.0 : 0.0);
-            if (cost < best - 1e-9) { best = cost; ks = cand; }
+        // the whole workspace within the budget when it can be: tables of all n inner indices if they fit
+        // beside the fixed parts (imported B, plans, rank, split-k partials), else chunks of kc with at most
+        // kChunkSplits partial sums and the chunk's imported rows
+        const size_t per_k = byte_table_bytes_per_k(l, w);
+        const size_t slot = 2 * (size_t)kPtWords * 4 * (size_t)m * l;     // one set of partial sums
+        const size_t fixed0 = off + align256((size_t)n * sizeof(ColPlan)) + align256((size_t)n * m) + 4096;
+        const int ks_full = choose_ksplit(m, n, l, w);
+        int kc = n;
+        if (fixed0 + (ks_full > 1 ? ks_full * slot : 0) + (size_t)n * per_k > byte_budget()) {
+            constexpr int kChunkSplits = 4;
+            const size_t fixed = fixed0 + kChunkSplits * slot;
+            const size_t per_kc = per_k + (size_t)l * 2 * kPtWords * 4;
+            kc = (int)std::min<size_t>(n, std::max<size_t>(1, fixed < byte_budget() ? (byte_budget() - fixed) / per_kc : 1));
+            const int kch = w <= 4 ? accum_chunk(L.slots) : 0;        // whole k_accum table chunks
+            if (kch && kc > kch) kc -= kc % kch;
+            L.ksplit = std::min(kChunkSplits, choose_ksplit(m, kc, l, w));
+        } else {
+            L.ksplit = ks_full;
         }
-        if (const char *e = getenv("PCMM_KSPLIT")) {         // measurement override (tools/)
-            const int v = atoi(e);
-            if (v >= 1 && v <= n) ks = v;
-        }
-        L.ksplit = ks;
+        L.kc = kc;
         L.plans = off;
         off = align256(off + (size_t)n * sizeof(ColPlan));
         L.rank = off;
         off = align256(off + (size_t)n * m);
+        const size_t ccnt = (size_t)kc * l;
         L.tables = off;
-        off = align256(off + cnt * 2 * (size_t)kPtWords * L.slots * 4);
+        off = align256(off + ccnt * 2 * (size_t)kPtWords * L.slots * 4);
         // upper-level scratch of k_tables, then (reused) the affine tables of k_affine
         L.scratch = off;
-        off = align256(off + std::max(cnt * 2 * (size_t)kPtWords * 2 * L.maxup * 4,
-                                      cnt * 2 * (size_t)kAffWords * L.slots * 4));
-        if (ks > 1) {
+        off = align256(off + std::max(ccnt * 2 * (size_t)kPtWords * 2 * L.maxup * 4,
+                                      ccnt * 2 * (size_t)kAffWords * L.slots * 4));
+        if (L.ksplit > 1 || kc < n) {
             L.partial = off;
-            off = align256(off + (size_t)ks * 2 * kPtWords * 4 * (size_t)m * l);
+            off = align256(off + (size_t)L.ksplit * 2 * kPtWords * 4 * (size_t)m * l);
+        }
+        if (kc < n) {
+            L.bsoa_c = off;                // the chunk's imported rows
+            off = align256(off + ccnt * 2 * kPtWords * 4);
         }
     }
     L.total = off;
@@ -391,34 +436,50 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
     uint8_t *rank = ws + L.rank;
     uint32_t *tables = (uint32_t *)(ws + L.tables);
     LAUNCH("plan", s, launch_plan(A_d, m, n, w, is_signed, iters, plans, rank, status, s));
-    // consecutive-column tables (k_tables_fast): unsigned A, launches that fill the GPU
-    // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
-    // (k_tables_coz, default: the same columns, tables and affine conversion in one kernel; k_affine skips them)
-    const int amode = tables_coz_mode();
-    const int aff = !is_signed && iters >= 2 && (amode == 2 || (amode == 1 && 2LL * n * l >= 65536));
-    const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * n * l >= 65536);
-    LAUNCH("tables", s, launch_tables(bsoa, plans, n, l, iters, L.slots, L.maxup, is_signed, tables,
-                                            (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1)));
-    uint32_t *atables = (uint32_t *)(ws + L.scratch);
-    // after k_tables: the affine tables share the region of k_tables' upper-level scratch
-    if (fast == 2) {
-        LAUNCH("tables_coz", s, launch_tables_coz(bsoa, plans, n, l, iters, L.slots, tables, atables, s));
-    } else if (fast) {
-        LAUNCH("tables_fast", s, launch_tables_fast(bsoa, plans, n, l, iters, L.slots, tables, atables, s));
-    }
-    LAUNCH("affine", s, launch_affine(tables, 2LL * n * l * L.slots, atables, s, plans, n, l, L.slots, iters, fast,
-                                      status + 1));
     const int64_t cnt = (int64_t)m * l;
-    uint32_t *acc_out = L.ksplit == 1 ? out : (uint32_t *)(ws + L.partial);
-    const int64_t split_stride = L.ksplit == 1 ? 0 : 2LL * kPtWords * cnt;
-    if (w <= 4) {
-        LAUNCH("accum", s, launch_accum(atables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
-    } else {
-        LAUNCH("accum", s, launch_accum_global(atables, rank, m, n, l, L.slots, L.ksplit, acc_out, split_stride, s));
-    }
-    if (L.ksplit > 1) {
-        uint32_t *partial = (uint32_t *)(ws + L.partial);
-        LAUNCH("reduce", s, launch_reduce_splits(partial, L.ksplit, cnt, out, s));
+    const bool chunked = L.kc < n;
+    for (int k0 = 0; k0 < n; k0 += L.kc) {
+        // the chunk k0 .. k0 + nc - 1 as a sub-problem (m, nc, l): its plans, rank rows and imported rows
+        const int nc = std::min(L.kc, n - k0);
+        const ColPlan *pc = plans + k0;
+        const uint8_t *rc_ = rank + (size_t)k0 * m;
+        const uint32_t *bc = bsoa;
+        if (chunked) {
+            uint32_t *dst = (uint32_t *)(ws + L.bsoa_c);
+            CK(cudaMemcpy2DAsync(dst, (size_t)nc * l * 4, bsoa + (size_t)k0 * l, (size_t)n * l * 4, (size_t)nc * l * 4,
+                                 2 * kPtWords, cudaMemcpyDeviceToDevice, s),
+               "chunk rows");
+            bc = dst;
+        }
+        // consecutive-column tables (k_tables_fast): unsigned A, launches that fill the GPU
+        // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
+        // (k_tables_coz, default: the same columns, tables and affine conversion in one kernel; k_affine skips them)
+        const int amode = tables_coz_mode();
+        const int aff = !is_signed && iters >= 2 && (amode == 2 || (amode == 1 && 2LL * nc * l >= 65536));
+        const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * nc * l >= 65536);
+        LAUNCH("tables", s, launch_tables(bc, pc, nc, l, iters, L.slots, L.maxup, is_signed, tables,
+                                          (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1)));
+        uint32_t *atables = (uint32_t *)(ws + L.scratch);
+        // after k_tables: the affine tables share the region of k_tables' upper-level scratch
+        if (fast == 2) {
+            LAUNCH("tables_coz", s, launch_tables_coz(bc, pc, nc, l, iters, L.slots, tables, atables, s));
+        } else if (fast) {
+            LAUNCH("tables_fast", s, launch_tables_fast(bc, pc, nc, l, iters, L.slots, tables, atables, s));
+        }
+        LAUNCH("affine", s, launch_affine(tables, 2LL * nc * l * L.slots, atables, s, pc, nc, l, L.slots, iters, fast,
+                                          status + 1));
+        const int ks = chunked ? std::min(choose_ksplit(m, nc, l, w), L.ksplit) : L.ksplit;   // <= partial slots
+        uint32_t *acc_out = (ks == 1 && !chunked) ? out : (uint32_t *)(ws + L.partial);
+        const int64_t split_stride = (ks == 1 && !chunked) ? 0 : 2LL * kPtWords * cnt;
+        if (w <= 4) {
+            LAUNCH("accum", s, launch_accum(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s));
+        } else {
+            LAUNCH("accum", s, launch_accum_global(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s));
+        }
+        if (ks > 1 || chunked) {
+            uint32_t *partial = (uint32_t *)(ws + L.partial);
+            LAUNCH("reduce", s, launch_reduce_splits(partial, ks, cnt, out, s, chunked && k0 > 0));
+        }
     }
     return PCMM_OK;
 }

@@ -69,7 +69,9 @@ cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int
 int accum_global_ctas_per_sm();
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s);
-cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s);
+// out = sum of the ksplit partial sums (+ out itself when accumulate: the byte path's k-chunks)
+cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s,
+                                 bool accumulate = false);
 cudaError_t launch_schoolbook(const int8_t *A, int m, int n, int l, int w, int is_signed, const uint32_t *bsoa,
                               uint32_t *out, int *status, cudaStream_t s);
 // the XYZZ schoolbook (school.cu k_school_xyzz), launch_schoolbook with PCMM_SCHOOL_XYZZ=1

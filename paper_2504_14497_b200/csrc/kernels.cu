@@ -596,7 +596,8 @@ __global__ void __launch_bounds__(128, PCMM_TFAST_MINB)
 }
 
 // ------------------------------------------------------------ a5: split-k reduce
-__global__ void k_reduce(const uint32_t *__restrict__ partial, int ksplit, int64_t count, uint32_t *__restrict__ out) {
+__global__ void k_reduce(const uint32_t *__restrict__ partial, int ksplit, int64_t count, uint32_t *__restrict__ out,
+                         int accumulate) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2 * count) return;
     const int c = (int)(t / count);
@@ -606,6 +607,10 @@ __global__ void k_reduce(const uint32_t *__restrict__ partial, int ksplit, int64
     soa_load(acc, partial + (int64_t)c * kPtWords * count, count, e);
     for (int s = 1; s < ksplit; s++) {
         soa_load(q, partial + s * split_stride + (int64_t)c * kPtWords * count, count, e);
+        pt_add_nl(acc, acc, q);
+    }
+    if (accumulate) {                                      // the running output of earlier k-chunks
+        soa_load(q, out + (int64_t)c * kPtWords * count, count, e);
         pt_add_nl(acc, acc, q);
     }
     soa_store(out + (int64_t)c * kPtWords * count, count, e, acc);
@@ -954,8 +959,9 @@ cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n
     return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s) {
-    k_reduce<<<blocks_for(2 * count, 128), 128, 0, s>>>(partial, ksplit, count, out);
+cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s,
+                                 bool accumulate) {
+    k_reduce<<<blocks_for(2 * count, 128), 128, 0, s>>>(partial, ksplit, count, out, accumulate ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -48,6 +48,16 @@ def test_product_does_not_import_oracle():
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
 
 
+def test_byte_path_workspace_bounded():
+    # the Cussen byte path builds its tables in k-chunks when they would not fit the 2 GiB budget:
+    # every w <= 8 at the 512^3 config stays within it (all tables of 512^3 w = 8 would be ~21 GB)
+    from paper_2504_14497_b200 import pcmm
+    L = pcmm.load()
+    for w in range(1, 9):
+        assert L.pcmm_workspace_bytes(512, 512, 512, w, 1) <= 2 << 30, w
+    assert L.pcmm_workspace_bytes(256, 256, 256, 4, 1) < 512 << 20      # the headline run is not chunked
+
+
 def test_validation_without_gpu():
     # argument errors are detected on the host before any device work
     from paper_2504_14497_b200 import pcmm

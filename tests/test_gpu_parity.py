@@ -766,6 +766,36 @@ def test_xyzz_schoolbook_forced():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_byte_path_k_chunks_forced():
+    # a tiny table budget (PCMM_BYTE_BUDGET_MB=1) forces the byte path's k-chunking (tables built and
+    # consumed chunk by chunk, each chunk's sums added into the running output) on the every-output cases
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_BYTE_BUDGET_MB="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_c64_config or test_degenerate or test_consecutive_column or "
+                        "test_accumulator_exceptional or test_xyzz_level1"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_c512_w8_chunked_sampled():
+    # 512^3 at w = 8 (tables of all k would take ~21 GB): the default 2 GiB budget chunks k;
+    # sampled outputs vs the Eq. 5 closed form
+    cfg = synth.Config("w8", 512, 512, 512, 8, False, 0, 255, 888)
+    I = synth.make_instance(cfg)
+    sk, pk = P.keygen(cfg.seed)
+    ctd = P.encrypt(pk, cuda(I.B.reshape(-1).astype(np.int32)), cuda(I.r_be))
+    assert P.workspace_bytes(512, 512, 512, 8, P.CUSSEN) <= 2 << 30
+    out = P.pcmm(cuda(I.A), ctd, 512, 8, False, path=P.CUSSEN).cpu().numpy()
+    r = I.r_be.reshape(512, 512, 32)
+    g = np.random.default_rng(8)
+    for (i, j) in [(0, 0), (511, 511), (0, 511)] + [(int(g.integers(512)), int(g.integers(512))) for _ in range(5)]:
+        assert out[i * 512 + j].tobytes() == oracle.closed_form(I.x, I.A[i], I.B[:, j], r[:, j]), (i, j)
+
+
 def test_byte_block_scan_forced():
     # the byte path's block-scan table kernel (k_tables_scan) forced on the every-output cases
     import os
