@@ -265,7 +265,11 @@ PCMM_API int pcmm_profile_read(char *names_h, float *ms_h, int max);
 /* Batched field ops on 32-byte big-endian values (reduced mod p):
  * op 0 a+b, 1 a-b, 2 a*b, 3 a^-1 (divsteps), 4 -a, 5 a^2 (dedicated
  * squaring), 6 a*b (the alternate product form), 7 a^-1 (Fermat chain)
- * (all mod p).  out_d[count][32].                                          */
+ * (all mod p); the accumulate loop's almost-reduced forms on operands whose
+ * odd Montgomery forms below 2^256 - p are first replaced by form + p:
+ * 8 a*b, 9 a^2, 10 a+b, 11 a-b (results reduced mod p), 12 the zero test
+ * (out = 1 if a = 0 mod p else 2, as a plain 32-byte integer).
+ * out_d[count][32].                                                        */
 PCMM_API int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out_d, int64_t count, void *stream);
 /* Batched group ops on 64-byte canonical points: op 0 P+Q, 1 2P, 2 v*P
  * (v_d[e], |v| < 2^15), 3 k*P (k = 32-byte BE scalar in q_d[e][0..31]; 4-bit

@@ -826,7 +826,7 @@ int pcmm_profile_read(char *names_h, float *ms_h, int max) {
 
 int pcmm_test_field(int op, const uint8_t *a_d, const uint8_t *b_d, uint8_t *out_d, int64_t count, void *stream) {
     g_err.clear();
-    if (count < 0 || op < 0 || op > 7) return fail(PCMM_EINVAL, "bad op / count");
+    if (count < 0 || op < 0 || op > 12) return fail(PCMM_EINVAL, "bad op / count");
     if (count && (!a_d || !b_d || !out_d)) return fail(PCMM_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)stream;
     LAUNCH("test_field", s, launch_test_field(op, a_d, b_d, out_d, count, s));

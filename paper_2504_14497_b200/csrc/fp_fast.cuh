@@ -174,8 +174,10 @@ __device__ __forceinline__ void fe_prod_eo(uint32_t T[16], const fe &a, const fe
 #define PCMM_MUL_PRODUCT 1        // 1: even/odd product scanning, 0: operand scanning
 #endif
 
-// Montgomery reduction of a 512-bit T (T < p 2^256) to T 2^-256 mod p in [0, p)
-__device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) {
+// Montgomery reduction of a 512-bit T (T < 2^512) to T 2^-256 mod p: in [0, p)
+// (kLazy = false), or in [0, 2^256) (kLazy = true: "almost reduced", see below)
+template <bool kLazy = false>
+__device__ __forceinline__ void fe_redc_t(fe &r, uint32_t T[16]) {
     // ---- reduction, 64-bit quotient digits: -p^-1 = 1 mod 2^64 (p = -1 mod 2^96),
     // so round r (base b = 2r) takes q = T[b] + 2^32 T[b+1] and adds
     //   q p 2^(32b) = -q + q 2^96 + u 2^192,  u = q (2^64 - 2^32 + 1) < 2^128.
@@ -212,7 +214,28 @@ __device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) {
               "+r"(T[b + 9]), "=r"(E)
             : "r"(q0), "r"(q1), "r"(w1), "r"(w2), "r"(w3));
     }
-    // ---- result = E*2^256 + T[8..15] < 2p; subtract p if it is >= p
+    if (kLazy) {
+        // ---- result V = E 2^256 + T[8..15] < 2^256 + p.  Lazy: keep V mod 2^256 when E = 0,
+        // else V - p = T[8..15] + (2^256 - p) (< 2^256 because then T[8..15] < p):
+        // 2^256 - p = (1, 0, 0, ffffffff, ffffffff, ffffffff, fffffffe, 0) little-endian words.
+        // One masked add chain instead of a subtraction and eight selects.
+        const uint32_t m = 0u - E;
+        asm("add.cc.u32 %0, %8, %16;\n\t"
+            "addc.cc.u32 %1, %9, 0;\n\t"
+            "addc.cc.u32 %2, %10, 0;\n\t"
+            "addc.cc.u32 %3, %11, %17;\n\t"
+            "addc.cc.u32 %4, %12, %17;\n\t"
+            "addc.cc.u32 %5, %13, %17;\n\t"
+            "addc.cc.u32 %6, %14, %18;\n\t"
+            "addc.u32 %7, %15, 0;"
+            : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]),
+              "=r"(r.v[7])
+            : "r"(T[8]), "r"(T[9]), "r"(T[10]), "r"(T[11]), "r"(T[12]), "r"(T[13]), "r"(T[14]), "r"(T[15]),
+              "r"(m & 1u), "r"(m), "r"(m & 0xfffffffeu));
+        return;
+    }
+    // ---- result = E*2^256 + T[8..15] < 2^256 + p (< 2p for inputs < p); subtract p if it is >= p
+    // (inputs < 2^256 but not < p give E = 1 with T[8..15] < p: the same subtraction is exact)
     uint32_t t[8], m;
     asm("sub.cc.u32 %0, %9, 0xffffffff;\n\t"
         "subc.cc.u32 %1, %10, 0xffffffff;\n\t"
@@ -229,6 +252,8 @@ __device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) {
 #pragma unroll
     for (int k = 0; k < 8; k++) r.v[k] = (T[8 + k] & m) | (t[k] & ~m);
 }
+
+__device__ __forceinline__ void fe_redc_fast(fe &r, uint32_t T[16]) { fe_redc_t<false>(r, T); }
 
 #ifndef PCMM_REDC_FAKE
 #define PCMM_REDC_FAKE 0        // MEASUREMENT ONLY (wrong results): 1 skips the reduction, 2 also the final subtraction
@@ -264,6 +289,109 @@ __device__ __forceinline__ void fe_mul_fast_v(fe &r, const fe &a, const fe &b) {
 
 __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) { fe_mul_fast_v<PCMM_MUL_PRODUCT>(r, a, b); }
 
+// ---- "almost reduced" (lazy) arithmetic for the accumulate loop: operands and
+// results anywhere in [0, 2^256) (congruent mod p, not canonical).  The product
+// skips the final conditional subtraction (fe_redc_t<true>), the sum folds its
+// carry back as + (2^256 - p), the difference adds p (twice in the rare case
+// b - a > p); an element is zero iff it is 0 or p.  Canonical values are
+// produced again by any non-lazy product (fe_mul_fast accepts inputs < 2^256).
+__device__ __forceinline__ void fe_mul_lz(fe &r, const fe &a, const fe &b) {
+    uint32_t T[16];
+    fe_prod_eo(T, a, b);
+    fe_redc_t<true>(r, T);
+}
+
+__device__ __forceinline__ bool fe_is_zero_lz(const fe &a) {
+    const uint32_t z = a.v[0] | a.v[1] | a.v[2] | a.v[3] | a.v[4] | a.v[5] | a.v[6] | a.v[7];
+    const uint32_t pp = ~a.v[0] | ~a.v[1] | ~a.v[2] | a.v[3] | a.v[4] | a.v[5] | (a.v[6] ^ 1u) | ~a.v[7];
+    return z == 0 || pp == 0;
+}
+
+// r = a + b (mod p), a, b, r in [0, 2^256)
+__device__ __forceinline__ void fe_add_lz(fe &r, const fe &a, const fe &b) {
+    uint32_t s[8], c;
+    asm("add.cc.u32 %0, %9, %17;\n\t"
+        "addc.cc.u32 %1, %10, %18;\n\t"
+        "addc.cc.u32 %2, %11, %19;\n\t"
+        "addc.cc.u32 %3, %12, %20;\n\t"
+        "addc.cc.u32 %4, %13, %21;\n\t"
+        "addc.cc.u32 %5, %14, %22;\n\t"
+        "addc.cc.u32 %6, %15, %23;\n\t"
+        "addc.cc.u32 %7, %16, %24;\n\t"
+        "addc.u32 %8, 0, 0;"
+        : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]), "=r"(s[7]), "=r"(c)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    uint32_t m = 0u - c;                          // carry: + (2^256 - p)
+    asm("add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, 0;\n\t"
+        "addc.cc.u32 %2, %2, 0;\n\t"
+        "addc.cc.u32 %3, %3, %10;\n\t"
+        "addc.cc.u32 %4, %4, %10;\n\t"
+        "addc.cc.u32 %5, %5, %10;\n\t"
+        "addc.cc.u32 %6, %6, %11;\n\t"
+        "addc.cc.u32 %7, %7, 0;\n\t"
+        "addc.u32 %8, 0, 0;"
+        : "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]), "+r"(s[7]), "=r"(c)
+        : "r"(m & 1u), "r"(m), "r"(m & 0xfffffffeu));
+    if (c) {                                      // a second wrap: only when a + b - p >= 2^256 - (2^256 - p)
+        asm("add.cc.u32 %0, %0, 1;\n\t"
+            "addc.cc.u32 %1, %1, 0;\n\t"
+            "addc.cc.u32 %2, %2, 0;\n\t"
+            "addc.cc.u32 %3, %3, 0xffffffff;\n\t"
+            "addc.cc.u32 %4, %4, 0xffffffff;\n\t"
+            "addc.cc.u32 %5, %5, 0xffffffff;\n\t"
+            "addc.cc.u32 %6, %6, 0xfffffffe;\n\t"
+            "addc.u32 %7, %7, 0;"
+            : "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]), "+r"(s[7]));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = s[k];
+}
+
+// r = a - b (mod p), a, b, r in [0, 2^256)
+__device__ __forceinline__ void fe_sub_lz(fe &r, const fe &a, const fe &b) {
+    uint32_t d[8], m, c;
+    asm("sub.cc.u32 %0, %9, %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32 %8, 0, 0;"
+        : "=&r"(d[0]), "=&r"(d[1]), "=&r"(d[2]), "=&r"(d[3]), "=&r"(d[4]), "=&r"(d[5]), "=&r"(d[6]), "=&r"(d[7]),
+          "=&r"(m)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    // borrow: + p (limbs m, m, m, 0, 0, 0, m & 1, m); carry out c = 1 iff the result is now >= 0
+    asm("add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %9;\n\t"
+        "addc.cc.u32 %2, %2, %9;\n\t"
+        "addc.cc.u32 %3, %3, 0;\n\t"
+        "addc.cc.u32 %4, %4, 0;\n\t"
+        "addc.cc.u32 %5, %5, 0;\n\t"
+        "addc.cc.u32 %6, %6, %10;\n\t"
+        "addc.cc.u32 %7, %7, %9;\n\t"
+        "addc.u32 %8, 0, 0;"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]), "+r"(d[6]), "+r"(d[7]), "=r"(c)
+        : "r"(m), "r"(m & 1u));
+    if (m & ~(0u - c)) {                          // still negative (b - a > p: only for b >= p): + p again
+        asm("add.cc.u32 %0, %0, 0xffffffff;\n\t"
+            "addc.cc.u32 %1, %1, 0xffffffff;\n\t"
+            "addc.cc.u32 %2, %2, 0xffffffff;\n\t"
+            "addc.cc.u32 %3, %3, 0;\n\t"
+            "addc.cc.u32 %4, %4, 0;\n\t"
+            "addc.cc.u32 %5, %5, 0;\n\t"
+            "addc.cc.u32 %6, %6, 1;\n\t"
+            "addc.u32 %7, %7, 0xffffffff;"
+            : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]), "+r"(d[6]), "+r"(d[7]));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) r.v[k] = d[k];
+}
+
 // ---- squaring: the 28 cross products a_i a_j (i < j) once, in the even/odd
 // accumulators (row i: j - i odd -> O, j - i even -> E; chains of 1..4 pairs),
 // C = E + O 2^32, T = 2 C + sum a_i^2 2^(64 i) (the diagonal as one fused
@@ -293,7 +421,8 @@ __device__ __forceinline__ void fe_mul_fast(fe &r, const fe &a, const fe &b) { f
         : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3), "+r"(d4), "+r"(d5), "+r"(c) \
         : "r"(x0), "r"(x1), "r"(x2), "r"(y))
 
-__device__ __forceinline__ void fe_sqr_fast(fe &r, const fe &a) {
+template <bool kLazy>
+__device__ __forceinline__ void fe_sqr_fast_t(fe &r, const fe &a) {
     const uint32_t a0 = a.v[0], a1 = a.v[1], a2 = a.v[2], a3 = a.v[3];
     const uint32_t a4 = a.v[4], a5 = a.v[5], a6 = a.v[6], a7 = a.v[7];
     uint32_t E[16], O[16];                       // E[k] = word k (k >= 2), O[k] = word k + 1
@@ -372,8 +501,11 @@ __device__ __forceinline__ void fe_sqr_fast(fe &r, const fe &a) {
         : "+r"(T[0]), "+r"(T[1]), "+r"(T[2]), "+r"(T[3]), "+r"(T[4]), "+r"(T[5]), "+r"(T[6]), "+r"(T[7]),
           "+r"(T[8]), "+r"(T[9]), "+r"(T[10]), "+r"(T[11]), "+r"(T[12]), "+r"(T[13]), "+r"(T[14]), "+r"(T[15])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7));
-    fe_redc_fast(r, T);
+    fe_redc_t<kLazy>(r, T);
 }
+
+__device__ __forceinline__ void fe_sqr_fast(fe &r, const fe &a) { fe_sqr_fast_t<false>(r, a); }
+__device__ __forceinline__ void fe_sqr_lz(fe &r, const fe &a) { fe_sqr_fast_t<true>(r, a); }
 
 
 // r = a + b mod p (a, b < p)
@@ -584,6 +716,34 @@ __device__ PCMM_HOTCALL fe3 fe_mul3_hot(const fe a0, const fe b0, const fe a1, c
     fe_mul_fast(r.x, a0, b0);
     fe_mul_fast(r.y, a1, b1);
     fe_mul_fast(r.z, a2, b2);
+    return r;
+}
+
+// lazy (almost reduced) forms of the software-pipelined XYZZ step's product groups (jac.cuh)
+__device__ PCMM_HOTCALL fe2 fe_mulsqr_lz_hot(const fe a, const fe b, const fe c) {
+    fe2 r;
+    fe_mul_lz(r.x, a, b);
+    fe_sqr_lz(r.y, c);
+    return r;
+}
+
+__device__ PCMM_HOTCALL fe4 fe_sqr_mul3_lz_hot(const fe c, const fe a0, const fe b0, const fe a1, const fe b1,
+                                               const fe a2, const fe b2) {
+    fe4 r;
+    fe_sqr_lz(r.x, c);
+    fe_mul_lz(r.y, a0, b0);
+    fe_mul_lz(r.z, a1, b1);
+    fe_mul_lz(r.w, a2, b2);
+    return r;
+}
+
+__device__ PCMM_HOTCALL fe4 fe_mul4_lz_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
+                                           const fe b2, const fe a3, const fe b3) {
+    fe4 r;
+    fe_mul_lz(r.x, a0, b0);
+    fe_mul_lz(r.y, a1, b1);
+    fe_mul_lz(r.z, a2, b2);
+    fe_mul_lz(r.w, a3, b3);
     return r;
 }
 

@@ -28,6 +28,14 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #ifndef PCMM_ACCUM_CHUNK_SLOTS
 #define PCMM_ACCUM_CHUNK_SLOTS 512  // table slots staged per chunk: k-chunk = this / 2^w (32 at w = 4)
 #endif
+#ifndef PCMM_ACC_LAZY
+// 1: almost-reduced values in the pipelined step (jac.cuh xyzz_add_aff_pipe_lz: no final conditional
+// subtraction in the products, lazy sums / differences).  Measured 8 % slower at 256^3 (3.95 vs
+// 3.67 ms): the rare second-correction branches of the lazy add / subtract split the straight-line
+// step into basic blocks that ptxas no longer interleaves, and the masked fold-back costs about what
+// the subtraction saved.  Kept as a measured variant (parity-tested by test_lazy_field_ops).
+#define PCMM_ACC_LAZY 0
+#endif
 #ifndef PCMM_ACC_PIPE
 #define PCMM_ACC_PIPE 1         // software-pipelined XYZZ step (jac.cuh xyzz_add_aff_pipe); needs PCMM_ACC_XYZZ
 #endif
@@ -143,7 +151,11 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
                 const uint32_t *T = tsm + (more ? kn * TWS + rsm[kn * ROWS + tid] * EW : kk * TWS + rsm[kk * ROWS + tid] * EW);
                 fe xn, yn;
                 ld_entry<EW>(xn, yn, T);
+#if PCMM_ACC_LAZY
+                xyzz_add_aff_pipe_lz(acc, x2, y2, U2, have_u2, xn);
+#else
                 xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);
+#endif
                 if (!more) break;
                 x2 = xn;
                 y2 = yn;

@@ -381,6 +381,45 @@ __device__ __forceinline__ void xyzz_add_aff_pipe(xyzz &A, const fe &x2, const f
 #endif
 }
 
+// The same step on almost-reduced values (fp_fast.cuh fe_*_lz: the accumulator,
+// U2 and every intermediate anywhere in [0, 2^256), products without the final
+// conditional subtraction).  Table entries are canonical; the exceptional path
+// and xyzz_to_proj use non-lazy products, whose outputs are canonical again.
+// P = 0 is tested as P in {0, p}.
+__device__ __forceinline__ void xyzz_add_aff_pipe_lz(xyzz &A, const fe &x2, const fe &y2, fe &U2, bool &have_u2,
+                                                     const fe &xn) {
+#ifdef __CUDA_ARCH__
+    if (A.inf | aff_is_inf(x2)) {
+        A = xyzz_add_slow(A, x2, y2);
+        have_u2 = false;
+        return;
+    }
+    if (!have_u2) U2 = fe_mul_call(x2, A.ZZ);
+    fe P, R;
+    fe_sub_lz(P, U2, A.X);
+    if (fe_is_zero_lz(P)) {
+        A = xyzz_add_slow(A, x2, y2);
+        have_u2 = false;
+        return;
+    }
+    const fe2 sp = fe_mulsqr_lz_hot(y2, A.ZZZ, P);           // S2 = y2 ZZZ, PP = P^2
+    fe_sub_lz(R, sp.x, A.Y);
+    const fe4 t = fe_sqr_mul3_lz_hot(R, P, sp.y, A.X, sp.y, A.ZZ, sp.y);   // R^2, PPP, Q = X1 PP, ZZ3
+    fe X3, Q2, D;
+    fe_add_lz(Q2, t.z, t.z);
+    fe_sub_lz(X3, t.x, t.y);
+    fe_sub_lz(X3, X3, Q2);                                   // X3 = R^2 - PPP - 2Q
+    fe_sub_lz(D, t.z, X3);
+    const fe4 u = fe_mul4_lz_hot(R, D, A.Y, t.y, A.ZZZ, t.y, xn, t.w);   // R (Q - X3), Y1 PPP, ZZZ3, U2'
+    fe_sub_lz(A.Y, u.x, u.y);
+    A.X = X3;
+    A.ZZ = t.w;
+    A.ZZZ = u.z;
+    U2 = u.w;
+    have_u2 = true;
+#endif
+}
+
 // The accumulate kernels' accumulator (hot.cu): PCMM_ACC_XYZZ=1 (default) XYZZ
 // (8M + 2S per step), 0 the Jacobian step above (9M + 2S).
 #ifndef PCMM_ACC_XYZZ

@@ -820,6 +820,17 @@ __global__ void k_decrypt(const __grid_constant__ Scalar8 x, const uint8_t *__re
 }
 
 // ------------------------------------------------------------ test hooks
+// x + p without reduction (x < 2^256 - p): the non-canonical representative of x
+__device__ __forceinline__ void fe_add_portable_nored(fe &r, const fe &x) {
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const uint64_t t = (uint64_t)x.v[i] + p_limb(i) + c;
+        r.v[i] = (uint32_t)t;
+        c = t >> 32;
+    }
+}
+
 __global__ void k_test_field(int op, const uint8_t *__restrict__ a, const uint8_t *__restrict__ b,
                              uint8_t *__restrict__ out, int64_t count) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -838,6 +849,24 @@ __global__ void k_test_field(int op, const uint8_t *__restrict__ a, const uint8_
         case 5: fe_sqr_fast(r, x); break;
         case 6: fe_mul_fast_v<1 - PCMM_MUL_PRODUCT>(r, x, y); break;
         case 7: fe_inv_fermat(r, x); break;
+        // lazy (almost-reduced) arithmetic: inputs whose Montgomery form is odd and below 2^256 - p are
+        // denormalised to form + p (in [p, 2^256)) first; outputs fully reduced by fe_from_mont below
+        case 8: case 9: case 10: case 11: case 12: {
+            fe xd = x, yd = y;
+            if (x.v[7] == 0 && x.v[6] < 0xfffffffeu && (x.v[0] & 1u)) fe_add_portable_nored(xd, x);   // odd forms
+            if (y.v[7] == 0 && y.v[6] < 0xfffffffeu && (y.v[0] & 1u)) fe_add_portable_nored(yd, y);
+            if (op == 8) fe_mul_lz(r, xd, yd);
+            else if (op == 9) fe_sqr_lz(r, xd);
+            else if (op == 10) fe_add_lz(r, xd, yd);
+            else if (op == 11) fe_sub_lz(r, xd, yd);
+            else {
+                fe_zero(r);
+                r.v[0] = fe_is_zero_lz(xd) ? 1u : 2u;
+                fe_to_be_bytes(out + e * 32, r);              // raw flag, not a field element
+                return;
+            }
+            break;
+        }
 #endif
         default: fe_neg(r, x); break;
     }

@@ -65,6 +65,33 @@ def test_field_ops_bit_exact():
             assert int.from_bytes(out[i].tobytes(), "big") == exp, (op, i)
 
 
+def test_lazy_field_ops():
+    # the accumulate loop's almost-reduced arithmetic (fp_fast.cuh fe_*_lz): operands in [0, 2^256),
+    # including non-canonical representatives x + p (ops 8-12 denormalise odd Montgomery forms below
+    # 2^256 - p); results must be congruent mod p (fully reduced by the harness afterwards), and the
+    # zero test must accept both 0 and p.  Edge forms: 0, 1, the largest below 2^256 - p (double wrap
+    # of the sum: both operands near 2^256), small even minus small odd (difference below -p).
+    Pm = ecref.P
+    R = 2**256
+    Rinv = pow(R, -1, Pm)
+    delta = R - Pm
+    forms = [0, 1, 2, 3, delta - 1, delta - 2, delta - 3, delta - 5, 5, 7, Pm - 1, Pm - 2]
+    forms += [rng.randrange(delta) for _ in range(1500)] + [rng.randrange(Pm) for _ in range(1500)]
+    a = [f * Rinv % Pm for f in forms]                      # plain values whose Montgomery forms are `forms`
+    b = [a[(i * 7 + 3) % len(a)] for i in range(len(a))]
+    b[: 12] = [a[4], a[4], a[6], a[2], a[4], a[0], a[1], a[3], a[6], a[0], a[11], a[10]]
+    A = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in a), dtype=np.uint8).reshape(-1, 32))
+    B = cuda(np.frombuffer(b"".join(v.to_bytes(32, "big") for v in b), dtype=np.uint8).reshape(-1, 32))
+    for op, f in [(8, lambda x, y: x * y % Pm), (9, lambda x, y: x * x % Pm), (10, lambda x, y: (x + y) % Pm),
+                  (11, lambda x, y: (x - y) % Pm)]:
+        out = P.test_field(op, A, B).cpu().numpy()
+        for i in range(len(a)):
+            assert int.from_bytes(out[i].tobytes(), "big") == f(a[i], b[i]), (op, i)
+    out = P.test_field(12, A, B).cpu().numpy()
+    for i in range(len(a)):
+        assert int.from_bytes(out[i].tobytes(), "big") == (1 if a[i] == 0 else 2), i
+
+
 def _pts(scalars):
     return cuda(np.frombuffer(b"".join(ecref.mulG(s) for s in scalars), dtype=np.uint8).reshape(-1, 64))
 
