@@ -16,6 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpcmm.so")
+# checked variant (PCMM_CHECKED=1: device-side bounds checks, pcmm.py loads it when PCMM_LIB_VARIANT=checked)
+LIB_CHECKED = os.path.join(HERE, "libpcmm_checked.so")
+BUILD_CHECKED = os.path.join(HERE, "_build_checked")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 UNITS = ["hot.cu", "kernels.cu", "affine.cu", "taff.cu", "school.cu", "strassen.cu", "wide.cu", "next2.cu", "paillier.cu", "api.cu"]
 # per-unit ptxas options (measured: k_affine 256^3 0.289 -> 0.261 ms at -O1; the other units want -O3)
@@ -39,23 +42,27 @@ def _deps():
     return out
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(checked: bool = False) -> bool:
+    lib = LIB_CHECKED if checked else LIB
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    bdir = BUILD_CHECKED if checked else BUILD
+    if not force and not needs_build(checked):
+        return lib
     nvcc = _nvcc()
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(bdir, exist_ok=True)
+    extra = ["-DPCMM_CHECKED=1"] if checked else []
 
     def compile_unit(u):
-        obj = os.path.join(BUILD, u.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *FLAGS, *UNIT_FLAGS.get(u, []), *os.environ.get("PCMM_EXTRA_NVCC_FLAGS", "").split(),
-               "-c", os.path.join(CSRC, u), "-o", obj]
+        obj = os.path.join(bdir, u.replace(".cu", ".o"))
+        cmd = [nvcc, *ARCH, *FLAGS, *UNIT_FLAGS.get(u, []), *extra,
+               *os.environ.get("PCMM_EXTRA_NVCC_FLAGS", "").split(), "-c", os.path.join(CSRC, u), "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -68,15 +75,14 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
     if verbose:
         for _, err in results:
             sys.stderr.write(err)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + [o for o, _ in results]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -99,6 +99,7 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
         const int kk = t / (TW / 4), r = t % (TW / 4);
         const int slot = r / (kAffWords / 4), q4 = (r % (kAffWords / 4)) * 4;
         const uint4 v = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW)[r];
+        PCMM_DCHECK(kk < kc && kk * TWS + slot * EW + q4 + 3 < AccumCfg<S>::kChunk * TWS && k0 + kk < n);
         uint32_t *d = tsw + kk * TWS + slot * EW + q4;
         d[0] = v.x;
         d[1] = v.y;
@@ -107,7 +108,9 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
     }
     for (int t = tid; t < kc * ROWS; t += ROWS) {
         const int row = rb * ROWS + (t % ROWS);
+        PCMM_DCHECK(t < AccumCfg<S>::kChunk * ROWS);
         rsm[t] = row < m ? rank[(int64_t)(k0 + t / ROWS) * m + row] : (uint8_t)0;
+        PCMM_DCHECK(rsm[t] < S);
     }
 }
 
@@ -129,6 +132,7 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
     const int tid = (int)threadIdx.x;
     const int i = rb * ROWS + tid;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
+    PCMM_DCHECK(blockDim.x == ROWS && s < ksplit && c < 2);
     acc_t acc;
     acc_init(acc);
     for (int k0 = kb; k0 < ke; k0 += KCH) {
@@ -221,11 +225,13 @@ __global__ void __launch_bounds__(kRowsG, 3)
     while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
     if (k < ke) {
         fe x2, y2;
+        PCMM_DCHECK(rank[(int64_t)k * m + i] < S);
         load_aff(x2, y2, tb + k * tstride + rank[(int64_t)k * m + i] * kAffWords);
         while (true) {
             int kn = k + 1;
             while (kn < ke && rank[(int64_t)kn * m + i] == 0) kn++;
             fe xn, yn;
+            PCMM_DCHECK(kn >= ke || rank[(int64_t)kn * m + i] < S);
             if (kn < ke) load_aff(xn, yn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kAffWords);
             acc_add_aff(acc, x2, y2);
             if (kn >= ke) break;

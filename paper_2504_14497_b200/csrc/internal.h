@@ -132,3 +132,27 @@ int accum_rows();
 int accum_chunk(int slots);   // k per shared-memory table chunk of k_accum (2^w <= 16 slots)
 
 }  // namespace pcmm
+
+// ---------------------------------------------------------------- checked build
+// PCMM_CHECKED=1 (build.py build(checked=True) -> libpcmm_checked.so; pcmm.py loads it when
+// PCMM_LIB_VARIANT=checked): device-side bounds checks on the shared-memory staging and scans and on
+// the table / plan indices, standing in for compute-sanitizer (not available on the GPU pool).
+// A failed check prints its site and traps (the launch fails loudly: PCMM_ECUDA).
+#ifndef PCMM_CHECKED
+#define PCMM_CHECKED 0
+#endif
+#if PCMM_CHECKED
+#include <cstdio>
+#define PCMM_DCHECK(cond)                                                                          \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("PCMM_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                             \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define PCMM_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif

@@ -68,6 +68,7 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
         if (a < lo || a > hi) bad = true;
         else if (a != 0) {
             const int b = a + kBmOff;
+            PCMM_DCHECK(b >= 0 && (b >> 5) < 12);
 #pragma unroll
             for (int q = 0; q < 12; q++)
                 if ((b >> 5) == q) bm[q] |= 1u << (b & 31);
@@ -98,6 +99,7 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
             const int nv = ns;
             for (int e = 0; e < nv; e++) {
                 const int b = v[e] + kBmOff;
+                PCMM_DCHECK(b >= 0 && (b >> 5) < 32);
                 b2[b >> 5] |= 1u << (b & 31);
             }
             ns = 0;
@@ -105,6 +107,7 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
                 for (uint32_t x = b2[q]; x; x &= x - 1u) s[ns++] = (int16_t)(32 * q + __ffs(x) - 1 - kBmOff);
             for (int e = 0; e < nv; e++) P->ptr[lev - 2][e] = (uint8_t)bm_rank(b2, v[e] + kBmOff);   // R3
         }
+        PCMM_DCHECK(ns <= kPlanCap);
         P->n[lev - 1] = (int16_t)ns;
         if (lev < N) {                                          // differences, first element kept (R6)
             for (int e = 0; e < ns; e++) v[e] = (int16_t)(e == 0 ? s[0] : s[e] - s[e - 1]);
@@ -126,6 +129,7 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
 // Table entry (projective point) store, entry-major: 24 contiguous words per
 // slot, written as 6 x 16-byte vector stores.
 __device__ __forceinline__ void table_store(uint32_t *block, int slot, const pt &q) {
+    PCMM_DCHECK(slot >= 0 && slot < kPlanCap);
     uint4 *d = reinterpret_cast<uint4 *>(block + slot * kPtWords);
     d[0] = make_uint4(q.X.v[0], q.X.v[1], q.X.v[2], q.X.v[3]);
     d[1] = make_uint4(q.X.v[4], q.X.v[5], q.X.v[6], q.X.v[7]);
@@ -139,6 +143,7 @@ __device__ __forceinline__ void table_store(uint32_t *block, int slot, const pt 
 // i.e. j innermost so that a warp (32 consecutive j, same k) reads and writes
 // whole 128-byte lines; all indices are warp-uniform (same column plan).
 __device__ __forceinline__ void scr_store(uint32_t *scr, int64_t base, int e, int64_t l, const pt &q) {
+    PCMM_DCHECK(e >= 0 && e < 2 * 32);                       // two ping-pong levels of max_upper(w) <= 32
     uint32_t *d = scr + (base + (int64_t)e * kPtWords) * l;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
@@ -149,6 +154,7 @@ __device__ __forceinline__ void scr_store(uint32_t *scr, int64_t base, int e, in
 }
 
 __device__ __forceinline__ void scr_load(pt &q, const uint32_t *scr, int64_t base, int e, int64_t l) {
+    PCMM_DCHECK(e >= 0 && e < 2 * 32);
     const uint32_t *d = scr + (base + (int64_t)e * kPtWords) * l;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
@@ -204,6 +210,8 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     const ColPlan &pl = plans[k];
     if (skip_fast && col_consecutive(pl, N)) return;                 // k_tables_fast
+    if (pl.n[0] == 0) return;            // all-zero column: no table (k_affine writes its identity markers);
+                                         // its tracking pointers were never written (found by the checked build)
     uint32_t *blk = tables + (((int64_t)c * n + k) * l + j) * (int64_t)(kPtWords * S);
     uint32_t *sj = scr + j;
     const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;   // in units of l-strided words
@@ -261,6 +269,7 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t
 constexpr int kTScanT = 128;
 
 __device__ __forceinline__ void tsm_store(uint32_t *sm, int i, const pt &q) {
+    PCMM_DCHECK(i >= 0 && i < kTScanT);
 #pragma unroll
     for (int w = 0; w < 8; w++) {
         sm[(0 * 8 + w) * kTScanT + i] = q.X.v[w];
@@ -270,6 +279,7 @@ __device__ __forceinline__ void tsm_store(uint32_t *sm, int i, const pt &q) {
 }
 
 __device__ __forceinline__ void tsm_load(pt &q, const uint32_t *sm, int i) {
+    PCMM_DCHECK(i >= 0 && i < kTScanT);
 #pragma unroll
     for (int w = 0; w < 8; w++) {
         q.X.v[w] = sm[(0 * 8 + w) * kTScanT + i];
@@ -279,6 +289,7 @@ __device__ __forceinline__ void tsm_load(pt &q, const uint32_t *sm, int i) {
 }
 
 __device__ __forceinline__ void table_load(pt &q, const uint32_t *block, int slot) {
+    PCMM_DCHECK(slot >= 0 && slot < kPlanCap);
     const uint4 *d = reinterpret_cast<const uint4 *>(block + slot * kPtWords);
     const uint4 x0 = d[0], x1 = d[1], y0 = d[2], y1 = d[3], z0 = d[4], z1 = d[5];
     q.X = fe{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
@@ -293,6 +304,7 @@ __global__ void __launch_bounds__(kTScanT) k_tables_scan(const uint32_t *__restr
     __shared__ uint32_t sm[kPtWords * kTScanT];
     const int64_t t = blockIdx.x;                                       // table (c, k, j), j fastest
     const int tid = (int)threadIdx.x;
+    PCMM_DCHECK(blockDim.x == kTScanT && t < 2LL * n * l);
     const int j = (int)(t % l);
     const int k = (int)((t / l) % n);
     const int c = (int)(t / ((int64_t)l * n));
@@ -331,6 +343,7 @@ __global__ void __launch_bounds__(kTScanT) k_tables_scan(const uint32_t *__restr
         const int u0 = min(tid * E, nlv), u1 = min(u0 + E, nlv);
         pt run = id, g;
         for (int u = u0; u < u1; u++) {                                    // own run, inclusive
+            PCMM_DCHECK(src + pp[u] < 2 * maxup && dst + u < 2 * maxup + kPlanCap);
             scr_load(g, sj, sbase, src + pp[u], l);
             pt_add_nl(run, run, g);
             if (lev == 1) table_store(blk, u + 1, run);
@@ -414,6 +427,7 @@ __global__ void __launch_bounds__(128, PCMM_TABLES_MINB)
     const int64_t cnt = (int64_t)n * l;
     const ColPlan &pl = plans[k];
     if (skip_fast && col_consecutive(pl, N)) valid = false;          // k_tables_fast
+    if (pl.n[0] == 0) valid = false;                                   // all-zero column (pointers unset)
     uint32_t *sj = scr + j;
     const int64_t sbase = ((int64_t)c * n + k) * 2 * maxup * kPtWords;
     int src = 0, n2 = 0;

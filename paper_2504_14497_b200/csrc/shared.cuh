@@ -50,6 +50,7 @@ __device__ __forceinline__ void st_aff_inf(uint32_t *d) {
 template <bool kFermat>
 __device__ __forceinline__ fe cta_inverse(const fe &acc, fe *wtot, fe *winv) {
     const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+    PCMM_DCHECK(blockDim.x == 128);                    // wtot[4], winv[4]
     fe one;
     fe_one_mont(one);
     // warp-inclusive prefix (Q) and suffix (S) products of the lane products

@@ -81,6 +81,7 @@ __device__ __forceinline__ bool coz_chain(const uint32_t *__restrict__ bsoa, con
     const ColPlan &pl = plans[k];
     if (!col_consecutive(pl, N)) return false;
     const int n1 = pl.n[0];
+    PCMM_DCHECK(n1 < S && t < 2LL * n * l);
     uint32_t *ablk = atab + t * (int64_t)(kAffWords * S);              // table index (c n + k) l + j = t
     uint32_t *pblk = ptab + t * (int64_t)(kPtWords * S);
     st_aff_inf(ablk);                                                   // slot 0 = the identity

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(128, 3) k_tables_wide(const uint32_t *__restri
     pt_identity(id);
     wt_store(blk, 0, id);
     const int n1 = nl[0];
+    if (n1 == 0) return;                 // all-zero column: its tracking pointers were never written
     if (N == 1) {
         for (int u = 0; u < n1; u++) {
             pt e;

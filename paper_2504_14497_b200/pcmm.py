@@ -57,11 +57,13 @@ def load(build_if_needed: bool = True) -> ctypes.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            if build_if_needed and _build.needs_build():
-                _build.build()
-            if not os.path.exists(_build.LIB):
-                raise PCMMError(PCMM_ECUDA, f"{_build.LIB} is missing (run __graft_entry__.build())")
-            L = ctypes.CDLL(_build.LIB)
+            checked = os.environ.get("PCMM_LIB_VARIANT", "") == "checked"    # device bounds-check build
+            lib = _build.LIB_CHECKED if checked else _build.LIB
+            if build_if_needed and _build.needs_build(checked):
+                _build.build(checked=checked)
+            if not os.path.exists(lib):
+                raise PCMMError(PCMM_ECUDA, f"{lib} is missing (run __graft_entry__.build())")
+            L = ctypes.CDLL(lib)
             vp, sz, i64, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64
             L.pcmm_last_error.restype = ctypes.c_char_p
             L.pcmm_version.restype = ctypes.c_char_p

@@ -823,6 +823,27 @@ def test_c512_w8_chunked_sampled():
         assert out[i * 512 + j].tobytes() == oracle.closed_form(I.x, I.A[i], I.B[:, j], r[:, j]), (i, j)
 
 
+def test_checked_build():
+    # the device bounds-check build (libpcmm_checked.so, PCMM_CHECKED=1: shared-memory staging and scans,
+    # table slots, scratch entries, plan bitmaps, CTA-inverse layout) on the every-output cases and the
+    # forced variants (block scans, consecutive-table kernels, k-chunks, XYZZ schoolbook); a failed
+    # check traps the launch.  Stands in for compute-sanitizer memcheck, which the GPU pool does not run.
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_LIB_VARIANT="checked")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "(test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or test_consecutive_column "
+                        "or test_all_identity or test_accumulator_exceptional or test_xyzz_level1 or test_vector "
+                        "or test_wide_every_output or test_wide_chunked or test_strassen_every or test_plan_matches "
+                        "or test_extreme_values or test_forced or test_byte_path_k_chunks or test_paillier_every) "
+                        "and not test_checked_build"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "PCMM_DCHECK failed" not in r.stdout
+
+
 def test_byte_block_scan_forced():
     # the byte path's block-scan table kernel (k_tables_scan) forced on the every-output cases
     import os

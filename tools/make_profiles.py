@@ -1,6 +1,7 @@
 """Turn the gpurun_out/ artifacts of tools/prof_round.sh into committed summaries:
 profiles/<round>_launches.txt (kernel share of the step from the ncu launch list),
-profiles/<round>_ncu_<kernel>.txt (ncu --set full summary), profiles/traffic.json."""
+profiles/<round>_ncu_<kernel>.txt (ncu --set full summary), profiles/traffic.json (with the sha of the
+library the captures are of: bench.py reports roofline.traffic only for that build)."""
 import csv
 import io
 import json
@@ -69,16 +70,14 @@ def ncu_summary(rep, tag):
 
 launches()
 t_acc = ncu_summary(os.path.join(OUT, "prof_accum.ncu-rep"), "k_accum")
-t_tab = ncu_summary(os.path.join(OUT, "prof_tables.ncu-rep"), "k_tables_fast")
-t_aff = ncu_summary(os.path.join(OUT, "prof_affine.ncu-rep"), "k_affine")
+t_tab = ncu_summary(os.path.join(OUT, "prof_tables.ncu-rep"), "k_tables_coz")
 tj = os.path.join(PROF, "traffic.json")
-data = json.load(open(tj)) if os.path.exists(tj) else {}
-data.setdefault("c256", {})
+data = {}
+sha = open(os.path.join(OUT, "lib_sha.txt")).read().strip() if os.path.exists(os.path.join(OUT, "lib_sha.txt")) else None
+data["c256"] = {"lib_sha16": sha,
+                "source": f"ncu --set full capture ({rnd}), dram__bytes_read.sum + dram__bytes_write.sum per launch"}
 if t_acc:
     data["c256"]["accum_dram_bytes"] = t_acc
 if t_tab:
-    data["c256"]["tables_dram_bytes"] = t_tab
-if t_aff:
-    data["c256"]["affine_dram_bytes"] = t_aff
-data["c256"]["source"] = f"ncu --set full capture ({rnd}), dram__bytes_read.sum + dram__bytes_write.sum per launch"
+    data["c256"]["tables_coz_dram_bytes"] = t_tab
 json.dump(data, open(tj, "w"), indent=1)
