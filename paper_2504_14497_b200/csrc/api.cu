@@ -64,11 +64,11 @@ struct Layout {
 // wave count per unit of work, ceil(base*ks / resident) / ks, plus a small charge
 // per extra split (the k_reduce additions and per-CTA chunk overheads).
 static int choose_ksplit(int m, int n, int l, int w) {
-    const int rows = accum_rows();
+    const int rows = w <= 4 ? accum_rows(m) : 128;
     const int rowblocks = (m + rows - 1) / rows;
     const int64_t base = (int64_t)l * 2 * rowblocks;
     const int slots = table_slots(w);
-    const double resident = (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(slots) : accum_global_ctas_per_sm());
+    const double resident = (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(slots, rows) : accum_global_ctas_per_sm());
     // On the shared-memory path only splits whose k-range is a whole number of table chunks
     // are considered when there are any besides 1 (measured: 256^3 2 splits 4.306 ms vs 3 ragged
     // ones 4.323, 512^3 4 splits 24.50 vs 3: 24.88, ML 16 splits 2.88 vs 10: 2.92).
@@ -113,7 +113,7 @@ Layout layout(int m, int n, int l, int w, int path) {
     L.bsoa = off;
     off = align256(off + cnt * 2 * kPtWords * 4);
     if (path == PCMM_PATH_CUSSEN) {
-        L.rows = accum_rows();
+        L.rows = accum_rows(m);
         L.slots = table_slots(w);
         L.maxup = max_upper(w);
         // the whole workspace within the budget when it can be: tables of all n inner indices if they fit

@@ -60,9 +60,9 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #ifndef PCMM_ACC_EW
 #define PCMM_ACC_EW 17          // shared-memory words per 16-word table entry (17: odd stride; 20: 16-B vector loads)
 #endif
-template <int S>
+template <int S, int R = PCMM_ACC_ROWS>
 struct AccumCfg {
-    static constexpr int kRows = PCMM_ACC_ROWS;
+    static constexpr int kRows = R;
     static constexpr int kChunk = (PCMM_ACCUM_CHUNK_SLOTS / S) < 128 ? (PCMM_ACCUM_CHUNK_SLOTS / S) : 128;
     static constexpr int kTW = kAffWords * S;                      // words per table (global, entry-major)
     static constexpr int kEW = PCMM_ACC_EW;                        // shared-memory entry stride
@@ -88,18 +88,18 @@ __device__ __forceinline__ void ld_entry(fe &x, fe &y, const uint32_t *T) {
 
 // Stage one k-chunk: tables and the rank bytes of the CTA's rows.  Out of line so
 // that the staging code does not perturb the hot loop's register allocation.
-template <int S>
+template <int S, int R>
 __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank,
                                          uint4 *smem4, uint8_t *rsm, int m, int n, int l, int c, int j, int rb,
                                          int k0, int kc, int tid) {
-    constexpr int ROWS = AccumCfg<S>::kRows, TW = AccumCfg<S>::kTW;
-    constexpr int EW = AccumCfg<S>::kEW, TWS = AccumCfg<S>::kTWs;
+    constexpr int ROWS = AccumCfg<S, R>::kRows, TW = AccumCfg<S, R>::kTW;
+    constexpr int EW = AccumCfg<S, R>::kEW, TWS = AccumCfg<S, R>::kTWs;
     uint32_t *tsw = reinterpret_cast<uint32_t *>(smem4);
     for (int t = tid; t < kc * (TW / 4); t += ROWS) {
         const int kk = t / (TW / 4), r = t % (TW / 4);
         const int slot = r / (kAffWords / 4), q4 = (r % (kAffWords / 4)) * 4;
         const uint4 v = reinterpret_cast<const uint4 *>(tables + (((int64_t)c * n + (k0 + kk)) * l + j) * TW)[r];
-        PCMM_DCHECK(kk < kc && kk * TWS + slot * EW + q4 + 3 < AccumCfg<S>::kChunk * TWS && k0 + kk < n);
+        PCMM_DCHECK(kk < kc && kk * TWS + slot * EW + q4 + 3 < AccumCfg<S, R>::kChunk * TWS && k0 + kk < n);
         uint32_t *d = tsw + kk * TWS + slot * EW + q4;
         d[0] = v.x;
         d[1] = v.y;
@@ -108,18 +108,19 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
     }
     for (int t = tid; t < kc * ROWS; t += ROWS) {
         const int row = rb * ROWS + (t % ROWS);
-        PCMM_DCHECK(t < AccumCfg<S>::kChunk * ROWS);
+        PCMM_DCHECK(t < AccumCfg<S, R>::kChunk * ROWS);
         rsm[t] = row < m ? rank[(int64_t)(k0 + t / ROWS) * m + row] : (uint8_t)0;
         PCMM_DCHECK(rsm[t] < S);
     }
 }
 
-template <int S>
-__global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
+// R = rows per CTA (128, or 64 for m <= 64: twice the resident CTAs, no idle half-CTA)
+template <int S, int R>
+__global__ void __launch_bounds__(R, PCMM_ACCUM_MINB * (PCMM_ACC_ROWS / R))
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
             uint32_t *__restrict__ out, int64_t split_stride) {
-    constexpr int ROWS = AccumCfg<S>::kRows, KCH = AccumCfg<S>::kChunk;
-    constexpr int EW = AccumCfg<S>::kEW, TWS = AccumCfg<S>::kTWs;
+    constexpr int ROWS = AccumCfg<S, R>::kRows, KCH = AccumCfg<S, R>::kChunk;
+    constexpr int EW = AccumCfg<S, R>::kEW, TWS = AccumCfg<S, R>::kTWs;
     extern __shared__ uint4 smem4[];
     const uint32_t *tsm = reinterpret_cast<const uint32_t *>(smem4);
     uint8_t *rsm = reinterpret_cast<uint8_t *>(smem4) + (size_t)KCH * TWS * 4;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(AccumCfg<S>::kRows, PCMM_ACCUM_MINB)
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
-        stage_chunk<S>(tables, rank, smem4, rsm, m, n, l, c, j, rb, k0, kc, tid);
+        stage_chunk<S, R>(tables, rank, smem4, rsm, m, n, l, c, j, rb, k0, kc, tid);
         __syncthreads();
         // each lane walks its own nonzero entries (zeros are the identity, skipped)
         int kk = 0;
@@ -351,33 +352,53 @@ __global__ void __launch_bounds__(128) k_bench_fp_mul(int iters, uint32_t *__res
     for (int i = 0; i < 8; i++) out[t * 8 + i] = x[0].v[i] ^ x[1].v[i] ^ x[2].v[i] ^ x[3].v[i];
 }
 
-template <int S>
+template <int S, int R>
 static int ctas_per_sm_s() {
     int occ = 0;
-    cudaFuncSetAttribute(k_accum<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S>::kSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<S>, AccumCfg<S>::kRows, AccumCfg<S>::kSmem) !=
-            cudaSuccess ||
+    cudaFuncSetAttribute(k_accum<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S, R>::kSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_accum<S, R>, R, AccumCfg<S, R>::kSmem) != cudaSuccess ||
         occ <= 0)
         occ = 3;
     return occ;
 }
 
-// resident k_accum CTAs per SM for table slot count S = 2^w (wave-balanced split-k)
-int accum_ctas_per_sm(int slots) {
-    static int occ[17] = {0};
-    if (slots < 2 || slots > 16) slots = 16;
-    if (!occ[slots]) {
-        switch (slots) {
-            case 2: occ[slots] = ctas_per_sm_s<2>(); break;
-            case 4: occ[slots] = ctas_per_sm_s<4>(); break;
-            case 8: occ[slots] = ctas_per_sm_s<8>(); break;
-            default: occ[slots] = ctas_per_sm_s<16>(); break;
-        }
+// rows per k_accum CTA for m rows: 64 when m <= 64 (PCMM_ACC_SMALL=0 disables)
+int accum_rows(int m) {
+    static int small = -1;
+    if (small < 0) {
+        const char *e = getenv("PCMM_ACC_SMALL");
+        small = e ? atoi(e) : 1;
     }
-    return occ[slots];
+    return (small && m <= 64 && PCMM_ACC_ROWS == 128) ? 64 : AccumCfg<16>::kRows;
 }
 
-int accum_rows() { return AccumCfg<16>::kRows; }
+// resident k_accum CTAs per SM for table slot count S = 2^w and the CTA's rows (wave-balanced split-k)
+int accum_ctas_per_sm(int slots, int rows) {
+    static int occ[2][17] = {{0}};
+    if (slots < 2 || slots > 16) slots = 16;
+    const int r = rows == 64 && PCMM_ACC_ROWS == 128 ? 1 : 0;
+    if (!occ[r][slots]) {
+#if PCMM_ACC_ROWS == 128
+        if (r) {
+            switch (slots) {
+                case 2: occ[r][slots] = ctas_per_sm_s<2, 64>(); break;
+                case 4: occ[r][slots] = ctas_per_sm_s<4, 64>(); break;
+                case 8: occ[r][slots] = ctas_per_sm_s<8, 64>(); break;
+                default: occ[r][slots] = ctas_per_sm_s<16, 64>(); break;
+            }
+        } else
+#endif
+        {
+            switch (slots) {
+                case 2: occ[r][slots] = ctas_per_sm_s<2, PCMM_ACC_ROWS>(); break;
+                case 4: occ[r][slots] = ctas_per_sm_s<4, PCMM_ACC_ROWS>(); break;
+                case 8: occ[r][slots] = ctas_per_sm_s<8, PCMM_ACC_ROWS>(); break;
+                default: occ[r][slots] = ctas_per_sm_s<16, PCMM_ACC_ROWS>(); break;
+            }
+        }
+    }
+    return occ[r][slots];
+}
 
 int accum_chunk(int slots) {
     switch (slots) {
@@ -388,26 +409,36 @@ int accum_chunk(int slots) {
     }
 }
 
-template <int S>
+template <int S, int R>
 static cudaError_t launch_accum_s(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int ksplit,
                                   uint32_t *out, int64_t stride, cudaStream_t s) {
-    const int rowblocks = (m + AccumCfg<S>::kRows - 1) / AccumCfg<S>::kRows;
+    const int rowblocks = (m + R - 1) / R;
     const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
     cudaError_t err =
-        cudaFuncSetAttribute(k_accum<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S>::kSmem);
+        cudaFuncSetAttribute(k_accum<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S, R>::kSmem);
     if (err) return err;
-    k_accum<S><<<grid, AccumCfg<S>::kRows, AccumCfg<S>::kSmem, s>>>(tables, rank, m, n, l, ksplit, out, stride);
+    k_accum<S, R><<<grid, R, AccumCfg<S, R>::kSmem, s>>>(tables, rank, m, n, l, ksplit, out, stride);
     return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_accum_r(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
+                                  int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+    switch (slots) {
+        case 2: return launch_accum_s<2, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        case 4: return launch_accum_s<4, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        case 8: return launch_accum_s<8, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        default: return launch_accum_s<16, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+    }
 }
 
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
-    switch (slots) {
-        case 2: return launch_accum_s<2>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        case 4: return launch_accum_s<4>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        case 8: return launch_accum_s<8>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        default: return launch_accum_s<16>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-    }
+#if PCMM_ACC_ROWS == 128
+    if (accum_rows(m) == 64)
+        return launch_accum_r<64>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s);
+#endif
+    return launch_accum_r<PCMM_ACC_ROWS>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s);
 }
 
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s) {

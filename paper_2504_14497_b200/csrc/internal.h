@@ -96,7 +96,7 @@ cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters,
 int num_sms();
 cudaError_t run_strassen(const void *A, int a_is_i32, int m, int n, int l, int w, int is_signed,
                          const uint32_t *bsoa, int leaf, uint32_t *out, int *status, cudaStream_t s);
-int accum_ctas_per_sm(int slots);
+int accum_ctas_per_sm(int slots, int rows);   // resident k_accum CTAs per SM (rows per CTA: accum_rows(m))
 // NEXT-4 (paillier.cu): PC-MM mod n^2, L 32-bit limbs; off[] = workspace offsets
 // {consts (one, R^2, unit: 3L words), Montgomery ciphertexts, plans, rank, tables, scratch}
 bool paillier_limbs_ok(int L);
@@ -128,7 +128,7 @@ cudaError_t launch_accum_wide(const uint32_t *atables, const uint16_t *rank, int
                               int first, uint32_t *out, cudaStream_t s);
 cudaError_t launch_schoolbook_wide(const int32_t *A, int m, int n, int l, int w, int is_signed,
                                    const uint32_t *bsoa, uint32_t *out, int *status, cudaStream_t s);
-int accum_rows();
+int accum_rows(int m);   // rows of A per k_accum CTA (128; 64 for m <= 64)
 int accum_chunk(int slots);   // k per shared-memory table chunk of k_accum (2^w <= 16 slots)
 
 }  // namespace pcmm
@@ -143,16 +143,16 @@ int accum_chunk(int slots);   // k per shared-memory table chunk of k_accum (2^w
 #endif
 #if PCMM_CHECKED
 #include <cstdio>
-#define PCMM_DCHECK(cond)                                                                          \
+#define PCMM_DCHECK(...)                                                                           \
     do {                                                                                           \
-        if (!(cond)) {                                                                             \
-            printf("PCMM_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+        if (!(__VA_ARGS__)) {                                                                      \
+            printf("PCMM_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #__VA_ARGS__, __FILE__, __LINE__, \
                    (int)blockIdx.x, (int)threadIdx.x);                                             \
             __trap();                                                                              \
         }                                                                                          \
     } while (0)
 #else
-#define PCMM_DCHECK(cond) \
-    do {                  \
+#define PCMM_DCHECK(...) \
+    do {                 \
     } while (0)
 #endif

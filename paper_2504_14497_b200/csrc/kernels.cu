@@ -967,7 +967,7 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
         const char *e = getenv("PCMM_TABLES_XYZZ");
         x_env = e ? atoi(e) : 1;
     }
-    if (x_env && slots >= 128 && N >= 2) {    // w = 8, 256^3: 4.49 -> 4.31 ms; w = 6: 3 % slower
+    if (x_env && (slots >= 128 || x_env == 2) && N >= 2) {    // w = 8, 256^3: 4.49 -> 4.31 ms; w = 6: 3 % slower
         if (is_signed)
             k_tables_x<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables,
                                                                           scratch, fast);

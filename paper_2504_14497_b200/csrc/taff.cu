@@ -62,6 +62,9 @@ __device__ __forceinline__ void st_xy(uint32_t *d, const fe &x, const fe &y) {
 
 }  // namespace
 
+#ifndef PCMM_TCOZ_DISCARD
+#define PCMM_TCOZ_DISCARD 1     // discard.global.L2 the parked entries after the backward pass
+#endif
 #ifndef PCMM_TCOZ_MINB
 #define PCMM_TCOZ_MINB 4
 #endif
@@ -201,6 +204,14 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
                 fe_mul(zinv, zinv, lam);
             }
         }
+#if PCMM_TCOZ_DISCARD
+        // the parked (X, Y, lambda) and (prefix, Z) are dead: drop their L2 lines without writing them back
+        if ((S * kPtWords * 4) % 128 == 0) {
+            const char *base = reinterpret_cast<const char *>(pblk);
+            for (int o = 0; o < S * kPtWords * 4; o += 128)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + o) : "memory");
+        }
+#endif
     }
 }
 
