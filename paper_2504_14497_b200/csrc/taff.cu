@@ -60,8 +60,40 @@ __device__ __forceinline__ void st_xy(uint32_t *d, const fe &x, const fe &y) {
     st_x(d + 8, y);
 }
 
+// 1 / a for every lane of the warp with one field inversion (all 32 lanes active): inclusive prefix (Q)
+// and suffix (S) products by shuffles, the inverse of the warp total (every lane runs it on the same
+// value), then 1/a = inv(total) Q(lane - 1) S(lane + 1).  No block barrier, unlike cta_inverse.
+__device__ __forceinline__ fe warp_inverse(const fe &a, const fe &one) {
+    const int lane = (int)(threadIdx.x & 31);
+    fe Q = a, S = a;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const fe q = fe_shfl_up(Q, d), sv = fe_shfl_down(S, d);
+        fe qm, sm;
+        fe_mul(qm, Q, q);
+        fe_mul(sm, S, sv);
+        if (lane >= d) Q = qm;
+        if (lane + d < 32) S = sm;
+    }
+    fe tot;
+#pragma unroll
+    for (int i = 0; i < 8; i++) tot.v[i] = __shfl_sync(0xffffffffu, Q.v[i], 31);
+    fe ti;
+    fe_inv(ti, tot);
+    fe qprev = fe_shfl_up(Q, 1), snext = fe_shfl_down(S, 1);
+    if (lane == 0) qprev = one;
+    if (lane == 31) snext = one;
+    fe r;
+    fe_mul(r, ti, qprev);
+    fe_mul(r, r, snext);
+    return r;
+}
+
 }  // namespace
 
+#ifndef PCMM_TCOZ_WARPINV
+#define PCMM_TCOZ_WARPINV 0     // 1: one inversion per warp (no block barrier) instead of per CTA
+#endif
 #ifndef PCMM_TCOZ_DISCARD
 #define PCMM_TCOZ_DISCARD 1     // discard.global.L2 the parked entries after the backward pass
 #endif
@@ -175,7 +207,11 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
             fe_mul(acc, acc, Zf);
         }
     }
+#if PCMM_TCOZ_WARPINV
+    fe inv = warp_inverse(acc, one);                                    // 1 / (product of this thread's Zs)
+#else
     fe inv = cta_inverse<false>(acc, wtot, winv);                       // 1 / (product of this thread's Zs)
+#endif
     for (int g = batch - 1; g >= 0; g--) {
         const int64_t t = t0 + g * T;
         if (t >= total) continue;
