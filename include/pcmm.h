@@ -238,8 +238,11 @@ PCMM_API int pcmm_decrypt_bsgs(const uint8_t sk_h[32], const void *ctx_d, int lo
                                int64_t count, int64_t lo, int64_t hi, int64_t *m_d, int32_t *status_d,
                                void *stream);
 
-/* Decrypt: m_e = phi^-1(C2 - x C1) by an exact lookup in
- * the table { m G : lo <= m <= hi } (hi - lo < 2^26).  sk_h = x (32 B BE).
+/* Decrypt: m_e = phi^-1(C2 - x C1), the unique m in
+ * [lo, hi] with m G = C2 - x C1 (hi - lo < 2^26, |lo|, |hi| < 2^30), found by
+ * baby-step giant-step with a baby-step table of 2^b points built for this
+ * call (2^(2b) ~ count (hi - lo + 1); the kernels of pcmm_decrypt_bsgs).
+ * sk_h = x (32 B BE).
  * m_d[e] receives the message, status_d[e] = 0 or PCMM_EDECODE if no m in
  * [lo, hi] matches (m_d[e] = 0 then) or PCMM_ENOTONCURVE for a bad input.
  * Async (allocates its table stream-ordered on `stream`).

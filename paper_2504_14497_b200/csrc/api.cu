@@ -626,29 +626,26 @@ int pcmm_decrypt_small(const uint8_t sk_h[32], const uint8_t *ct_d, int64_t coun
         const uint8_t *p = sk_h + 28 - 4 * i;
         x[i] = ((uint32_t)p[0] << 24) | ((uint32_t)p[1] << 16) | ((uint32_t)p[2] << 8) | p[3];
     }
-    size_t sort_tmp = 0;
-    CK(sort_pairs(nullptr, sort_tmp, nullptr, nullptr, nullptr, nullptr, tc, s), "sort sizing");
-    const size_t o_k0 = 0, o_k1 = align256(tc * 8), o_i0 = o_k1 + align256(tc * 8), o_i1 = o_i0 + align256(tc * 4),
-                 o_pts = o_i1 + align256(tc * 4), o_tmp = o_pts + align256(tc * 64), total = o_tmp + align256(sort_tmp);
-    uint8_t *buf = nullptr;
-    CK(cudaMallocAsync((void **)&buf, total, s), "cudaMallocAsync");
-    uint64_t *k0 = (uint64_t *)(buf + o_k0), *k1 = (uint64_t *)(buf + o_k1);
-    uint32_t *i0 = (uint32_t *)(buf + o_i0), *i1 = (uint32_t *)(buf + o_i1);
-    uint8_t *pts = buf + o_pts;
+    // baby-step giant-step (next2.cu) with a baby-step table sized for this call: s ~ sqrt(count x range)
+    // balances the table build (s points) against the giant steps (range / s per ciphertext)
+    const uint64_t range = (uint64_t)tc;
+    int lb = 4;
+    while (lb < 22 && ((uint64_t)1 << (2 * lb)) < range * (uint64_t)std::min<int64_t>(count, 1 << 20)) lb++;
+    while ((range >> lb) > (1ULL << 24)) lb++;
+    uint8_t *ctx = nullptr;
+    CK(cudaMallocAsync((void **)&ctx, bsgs_ctx_bytes(lb), s), "cudaMallocAsync");
     int rc = PCMM_OK;
     do {
-        prof_begin("dlog_table", s);
-        cudaError_t e = launch_dlog_table(lo, tc, k0, i0, pts, s);
+        prof_begin("bsgs_init", s);
+        cudaError_t e = launch_bsgs_init(lb, (uint32_t *)ctx, s);
         prof_end(s);
-        if (e) { rc = cuda_fail(e, "dlog_table"); break; }
-        e = sort_pairs(buf + o_tmp, sort_tmp, k0, k1, i0, i1, tc, s);
-        if (e) { rc = cuda_fail(e, "sort"); break; }
+        if (e) { rc = cuda_fail(e, "bsgs_init"); break; }
         prof_begin("decrypt", s);
-        e = launch_decrypt(x, ct_d, count, lo, k1, i1, pts, tc, m_d, status_d, s);
+        e = launch_decrypt_bsgs(x, (const uint32_t *)ctx, ct_d, count, lo, hi, m_d, status_d, s);
         prof_end(s);
         if (e) { rc = cuda_fail(e, "decrypt"); break; }
     } while (0);
-    cudaFreeAsync(buf, s);
+    cudaFreeAsync(ctx, s);
     return rc;
 }
 

@@ -81,13 +81,6 @@ cudaError_t launch_normalize(const uint32_t *proj, int64_t count, uint8_t *ct, c
 cudaError_t launch_encrypt(const uint8_t *pk64, const int32_t *b, const uint8_t *r, int64_t count, uint8_t *ct,
                            cudaStream_t s);
 cudaError_t launch_pubkey(const uint32_t x[8], uint8_t *out64_d, cudaStream_t s);
-cudaError_t launch_dlog_table(int64_t lo, int64_t count, uint64_t *keys, uint32_t *idx, uint8_t *pts,
-                              cudaStream_t s);
-cudaError_t launch_decrypt(const uint32_t x[8], const uint8_t *ct, int64_t count, int64_t lo, const uint64_t *keys,
-                           const uint32_t *idx, const uint8_t *pts, int64_t tcount, int64_t *m, int32_t *status,
-                           cudaStream_t s);
-cudaError_t sort_pairs(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
-                       uint32_t *vout, int64_t count, cudaStream_t s);
 cudaError_t launch_test_field(int op, const uint8_t *a, const uint8_t *b, uint8_t *out, int64_t count,
                               cudaStream_t s);
 cudaError_t launch_test_point(int op, const uint8_t *p, const uint8_t *q, const int32_t *v, uint8_t *out,

@@ -11,8 +11,7 @@
 //   k_reduce       a5: split-k partial sums
 //   k_normalize    a6: batch inversion -> canonical affine bytes
 //   k_school       s1: schoolbook PC-MM
-//   k_encrypt / k_pubkey / k_dlog_table / k_decrypt: boundary
-#include <cub/device/device_radix_sort.cuh>
+//   k_encrypt / k_pubkey: boundary; decryption: next2.cu (BSGS)
 
 #include <algorithm>
 
@@ -762,76 +761,6 @@ __global__ void k_pubkey(const uint32_t x0, const uint32_t x1, const uint32_t x2
     store_canonical_point(out, H);
 }
 
-// table { m G : m = lo + t } with sort keys = first 8 bytes of the canonical bytes
-__global__ void k_dlog_table(int64_t lo, int64_t count, uint64_t *__restrict__ keys, uint32_t *__restrict__ idx,
-                             uint8_t *__restrict__ pts) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= count) return;
-    const int64_t mval = lo + t;
-    pt G, P;
-    generator_mont(G);
-    pt_mul_small(P, (int)mval, G);
-    uint8_t *dst = pts + t * 64;
-    store_canonical_point(dst, P);
-    const uint4 first = reinterpret_cast<const uint4 *>(dst)[0];
-    keys[t] = ((uint64_t)bswap32(first.x) << 32) | bswap32(first.y);
-    idx[t] = (uint32_t)t;
-}
-
-struct Scalar8 {
-    uint32_t k[8];
-};
-
-__global__ void k_decrypt(const __grid_constant__ Scalar8 x, const uint8_t *__restrict__ ct, int64_t count, int64_t lo,
-                          const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx,
-                          const uint8_t *__restrict__ pts, int64_t tcount, int64_t *__restrict__ mout,
-                          int32_t *__restrict__ status) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= count) return;
-    pt C1, C2, M;
-    bool ok = load_canonical_point(C1, ct + e * 128);
-    ok = load_canonical_point(C2, ct + e * 128 + 64) && ok;
-    if (!ok) {
-        mout[e] = 0;
-        status[e] = -4;
-        return;
-    }
-    uint32_t xk[8];                            // local copy (never index the param space)
-#pragma unroll
-    for (int i = 0; i < 8; i++) xk[i] = x.k[i];
-    pt_mul_scalar_win(M, xk, C1);             // C1 decoded: Z = 1 or the identity
-    pt_neg(M, M);
-    pt_add_nl(M, C2, M);                        // C2 - x C1 = phi(m)
-    __align__(16) uint8_t buf[64];
-    store_canonical_point(buf, M);
-    const uint4 first = reinterpret_cast<const uint4 *>(buf)[0];
-    const uint64_t key = ((uint64_t)bswap32(first.x) << 32) | bswap32(first.y);
-    int64_t a = 0, b = tcount;                 // lower bound of key
-    while (a < b) {
-        int64_t mid = (a + b) >> 1;
-        if (keys[mid] < key) a = mid + 1;
-        else b = mid;
-    }
-    int32_t st = -5;
-    int64_t mv = 0;
-    for (int64_t q = a; q < tcount && keys[q] == key; q++) {
-        const uint4 *cand = reinterpret_cast<const uint4 *>(pts + (int64_t)idx[q] * 64);
-        const uint4 *mine = reinterpret_cast<const uint4 *>(buf);
-        bool eq = true;
-#pragma unroll
-        for (int z = 0; z < 4; z++) {
-            uint4 u = cand[z], v = mine[z];
-            eq = eq && u.x == v.x && u.y == v.y && u.z == v.z && u.w == v.w;
-        }
-        if (eq) {
-            st = 0;
-            mv = lo + idx[q];
-            break;
-        }
-    }
-    mout[e] = mv;
-    status[e] = st;
-}
 
 // ------------------------------------------------------------ test hooks
 // x + p without reduction (x < 2^256 - p): the non-canonical representative of x
@@ -1046,26 +975,6 @@ cudaError_t launch_pubkey(const uint32_t x[8], uint8_t *out64_d, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_dlog_table(int64_t lo, int64_t count, uint64_t *keys, uint32_t *idx, uint8_t *pts,
-                              cudaStream_t s) {
-    k_dlog_table<<<blocks_for(count, 128), 128, 0, s>>>(lo, count, keys, idx, pts);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_decrypt(const uint32_t x[8], const uint8_t *ct, int64_t count, int64_t lo, const uint64_t *keys,
-                           const uint32_t *idx, const uint8_t *pts, int64_t tcount, int64_t *m, int32_t *status,
-                           cudaStream_t s) {
-    if (count == 0) return cudaSuccess;
-    Scalar8 xs;
-    for (int i = 0; i < 8; i++) xs.k[i] = x[i];
-    k_decrypt<<<blocks_for(count, 64), 64, 0, s>>>(xs, ct, count, lo, keys, idx, pts, tcount, m, status);
-    return cudaGetLastError();
-}
-
-cudaError_t sort_pairs(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
-                       uint32_t *vout, int64_t count, cudaStream_t s) {
-    return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)count, 0, 64, s);
-}
 
 cudaError_t launch_test_field(int op, const uint8_t *a, const uint8_t *b, uint8_t *out, int64_t count,
                               cudaStream_t s) {
