@@ -836,7 +836,9 @@ def test_checked_build():
                         "(test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or test_consecutive_column "
                         "or test_all_identity or test_accumulator_exceptional or test_xyzz_level1 or test_vector "
                         "or test_wide_every_output or test_wide_chunked or test_strassen_every or test_plan_matches "
-                        "or test_extreme_values or test_forced or test_byte_path_k_chunks or test_paillier_every) "
+                        "or test_extreme_values or test_forced or test_byte_path_k_chunks or test_paillier_every "
+                        "or test_full_size_comparison_paths_sampled or test_c512_w8_chunked_sampled "
+                        "or test_full_size_gpu_encrypted_inputs_sampled or test_wide_full_grid_size_sampled) "
                         "and not test_checked_build"],
                        env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
