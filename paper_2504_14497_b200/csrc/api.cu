@@ -458,7 +458,8 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         const int aff = !is_signed && iters >= 2 && (amode == 2 || (amode == 1 && 2LL * nc * l >= 65536));
         const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * nc * l >= 65536);
         LAUNCH("tables", s, launch_tables(bc, pc, nc, l, iters, L.slots, L.maxup, is_signed, tables,
-                                          (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1)));
+                                          (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1),
+                                          status + 1));
         uint32_t *atables = (uint32_t *)(ws + L.scratch);
         // after k_tables: the affine tables share the region of k_tables' upper-level scratch
         if (fast == 2) {

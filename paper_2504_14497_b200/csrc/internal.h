@@ -41,7 +41,8 @@ cudaError_t launch_plan(const int8_t *A, int m, int n, int w, int is_signed, int
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
                           int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s,
                           int skip_fast = 0,    // skip_fast: consecutive columns left to k_tables_fast
-                          int maxlen = 0);      // min(m, 2^w - 1): long tables of few launches -> block scan
+                          int maxlen = 0,       // min(m, 2^w - 1): long tables of few launches -> block scan
+                          const int *general = nullptr);   // k_plan's flag: no general column -> k_tables exits
 // homogeneous tables [c][k][j][slot][24] -> affine tables [c][k][j][slot][16] (batch inversion)
 // plans != nullptr: entries of consecutive columns (built by k_tables_fast) are skipped
 // plans != nullptr (byte path): per-column entry kinds (slot 0 / unused slots -> identity markers without

@@ -197,7 +197,8 @@ template <bool kSigned>
 __global__ void __launch_bounds__(128, PCMM_TABLES_MINB) k_tables(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
                                                    int n, int l, int N, int S, int maxup,
                                                    uint32_t *__restrict__ tables, uint32_t *__restrict__ scr,
-                                                   int skip_fast) {
+                                                   int skip_fast, const int *__restrict__ general) {
+    if (skip_fast && general != nullptr && *general == 0) return;      // every column consecutive (k_plan's flag)
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = 2LL * n * l;
     if (t >= total) return;
@@ -879,7 +880,8 @@ static int tables_fast_enabled() {
 }
 
 cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
-                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s, int fast, int maxlen) {
+                          int is_signed, uint32_t *tables, uint32_t *scratch, cudaStream_t s, int fast, int maxlen,
+                          const int *general) {
     // few tables (fewer than two per SM) of >= 16 entries (maxlen = min(m, 2^w - 1)): one CTA per
     // table with block-scan prefix sums (measured: at 8-15 entries the serial thread is faster)
     static int scan_env = -1;                                 // PCMM_TABLES_SCAN: 0 never, 1 auto, 2 always
@@ -907,10 +909,10 @@ cudaError_t launch_tables(const uint32_t *bsoa, const ColPlan *plans, int n, int
     }
     if (is_signed)
         k_tables<true><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables, scratch,
-                                                                    fast);
+                                                                    fast, general);
     else
         k_tables<false><<<blocks_for(2LL * n * l, 128), 128, 0, s>>>(bsoa, plans, n, l, N, slots, maxup, tables,
-                                                                     scratch, fast);
+                                                                     scratch, fast, general);
     return cudaGetLastError();
 }
 
