@@ -164,11 +164,17 @@ def paper_model_adds(A: np.ndarray, l: int, w: int) -> int:
 
 
 def lib_sha16() -> str | None:
+    """Identity of the library build: sha256 over its sources (csrc/, include/pcmm.h) and build.py (flags),
+    so that a rebuild of the same sources (e.g. the driver's build()) keeps the identity of an ncu capture."""
     import hashlib
     try:
         from paper_2504_14497_b200 import build as _b
-        with open(_b.LIB, "rb") as f:
-            return hashlib.sha256(f.read()).hexdigest()[:16]
+        h = hashlib.sha256()
+        for path in sorted(_b._deps()):
+            h.update(os.path.basename(path).encode())
+            with open(path, "rb") as f:
+                h.update(f.read())
+        return h.hexdigest()[:16]
     except Exception:
         return None
 
@@ -176,7 +182,7 @@ def lib_sha16() -> str | None:
 def dram_traffic(config_name: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per k_accum launch from an `ncu --set full` capture
     (profiles/traffic.json, written by tools/traffic.py from the .ncu-rep).  Used only when the capture
-    was taken of THIS libpcmm.so (same sha256): a number from another build is stale -> null."""
+    was taken of a library built from THESE sources (same source sha256): a number from other code is stale -> null."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             d = json.load(f)
