@@ -681,13 +681,28 @@ __device__ PCMM_HOTCALL fe2 fe_sqr2_hot(const fe a, const fe b) {
 }
 
 // (c^2, a0 b0, a1 b1, a2 b2) and four products: the software-pipelined XYZZ step
+#ifndef PCMM_SQRMUL3_IL
+#define PCMM_SQRMUL3_IL 0       // 1: the square as a general product in a phase-interleaved 4-product group
+#endif
+template <int K>
+__device__ __forceinline__ void fe_mul_il(fe *r, const fe *a, const fe *b);
 __device__ PCMM_HOTCALL fe4 fe_sqr_mul3_hot(const fe c, const fe a0, const fe b0, const fe a1, const fe b1,
                                             const fe a2, const fe b2) {
     fe4 r;
+#if PCMM_SQRMUL3_IL
+    const fe a[4] = {c, a0, a1, a2}, b[4] = {c, b0, b1, b2};
+    fe o[4];
+    fe_mul_il<4>(o, a, b);
+    r.x = o[0];
+    r.y = o[1];
+    r.z = o[2];
+    r.w = o[3];
+#else
     fe_sqr_fast(r.x, c);
     fe_mul_fast(r.y, a0, b0);
     fe_mul_fast(r.z, a1, b1);
     fe_mul_fast(r.w, a2, b2);
+#endif
     return r;
 }
 
@@ -700,13 +715,28 @@ __device__ PCMM_HOTCALL fe3 fe_sqr_mul2_hot(const fe c, const fe a0, const fe b0
     return r;
 }
 
+#ifndef PCMM_MUL4_IL
+#define PCMM_MUL4_IL 0          // 1: the 4-product group written phase by phase (fe_mul_il<4>, below)
+#endif
+template <int K>
+__device__ __forceinline__ void fe_mul_il(fe *r, const fe *a, const fe *b);
 __device__ PCMM_HOTCALL fe4 fe_mul4_hot(const fe a0, const fe b0, const fe a1, const fe b1, const fe a2,
                                         const fe b2, const fe a3, const fe b3) {
     fe4 r;
+#if PCMM_MUL4_IL
+    const fe a[4] = {a0, a1, a2, a3}, b[4] = {b0, b1, b2, b3};
+    fe o[4];
+    fe_mul_il<4>(o, a, b);
+    r.x = o[0];
+    r.y = o[1];
+    r.z = o[2];
+    r.w = o[3];
+#else
     fe_mul_fast(r.x, a0, b0);
     fe_mul_fast(r.y, a1, b1);
     fe_mul_fast(r.z, a2, b2);
     fe_mul_fast(r.w, a3, b3);
+#endif
     return r;
 }
 
@@ -745,6 +775,137 @@ __device__ PCMM_HOTCALL fe4 fe_mul4_lz_hot(const fe a0, const fe b0, const fe a1
     fe_mul_lz(r.z, a2, b2);
     fe_mul_lz(r.w, a3, b3);
     return r;
+}
+
+// ---- K independent products written phase by phase (all K products' E/O rows, then all merges, then
+// reduction round by round across the K products, then the K final subtractions), so that the
+// instruction stream ptxas starts from is already interleaved (PCMM_MUL4_IL: the accumulate step's
+// 4-product group).  Same arithmetic and results as K calls of fe_mul_fast.
+template <int K>
+__device__ __forceinline__ void fe_mul_il(fe *r, const fe *a, const fe *b) {
+    uint32_t E[K][16], O[K][16];
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint64_t pe = (uint64_t)a[q].v[2 * j] * b[q].v[0];
+            const uint64_t po = (uint64_t)a[q].v[2 * j + 1] * b[q].v[0];
+            E[q][2 * j] = (uint32_t)pe;
+            E[q][2 * j + 1] = (uint32_t)(pe >> 32);
+            O[q][2 * j] = (uint32_t)po;
+            O[q][2 * j + 1] = (uint32_t)(po >> 32);
+        }
+#pragma unroll
+        for (int k = 8; k < 16; k++) {
+            E[q][k] = 0;
+            O[q][k] = 0;
+        }
+    }
+#pragma unroll
+    for (int i = 1; i < 8; i++) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            const uint32_t bi = b[q].v[i];
+            const uint32_t a0 = a[q].v[0], a1 = a[q].v[1], a2 = a[q].v[2], a3 = a[q].v[3];
+            const uint32_t a4 = a[q].v[4], a5 = a[q].v[5], a6 = a[q].v[6], a7 = a[q].v[7];
+            if (i & 1) {
+                PCMM_CHAIN4C(O[q][i - 1], O[q][i], O[q][i + 1], O[q][i + 2], O[q][i + 3], O[q][i + 4], O[q][i + 5],
+                             O[q][i + 6], O[q][i + 7], a0, a2, a4, a6, bi);
+                if (i < 7) {
+                    PCMM_CHAIN4C(E[q][i + 1], E[q][i + 2], E[q][i + 3], E[q][i + 4], E[q][i + 5], E[q][i + 6],
+                                 E[q][i + 7], E[q][i + 8], E[q][(i + 9) & 15], a1, a3, a5, a7, bi);
+                } else {
+                    PCMM_CHAIN4(E[q][8], E[q][9], E[q][10], E[q][11], E[q][12], E[q][13], E[q][14], E[q][15], a1, a3,
+                                a5, a7, bi);
+                }
+            } else {
+                PCMM_CHAIN4C(E[q][i], E[q][i + 1], E[q][i + 2], E[q][i + 3], E[q][i + 4], E[q][i + 5], E[q][i + 6],
+                             E[q][i + 7], E[q][i + 8], a0, a2, a4, a6, bi);
+                PCMM_CHAIN4C(O[q][i], O[q][i + 1], O[q][i + 2], O[q][i + 3], O[q][i + 4], O[q][i + 5], O[q][i + 6],
+                             O[q][i + 7], O[q][i + 8], a1, a3, a5, a7, bi);
+            }
+        }
+    }
+    uint32_t T[K][16];
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+        T[q][0] = E[q][0];
+        asm("add.cc.u32 %0, %15, %30;\n\t"
+            "addc.cc.u32 %1, %16, %31;\n\t"
+            "addc.cc.u32 %2, %17, %32;\n\t"
+            "addc.cc.u32 %3, %18, %33;\n\t"
+            "addc.cc.u32 %4, %19, %34;\n\t"
+            "addc.cc.u32 %5, %20, %35;\n\t"
+            "addc.cc.u32 %6, %21, %36;\n\t"
+            "addc.cc.u32 %7, %22, %37;\n\t"
+            "addc.cc.u32 %8, %23, %38;\n\t"
+            "addc.cc.u32 %9, %24, %39;\n\t"
+            "addc.cc.u32 %10, %25, %40;\n\t"
+            "addc.cc.u32 %11, %26, %41;\n\t"
+            "addc.cc.u32 %12, %27, %42;\n\t"
+            "addc.cc.u32 %13, %28, %43;\n\t"
+            "addc.u32 %14, %29, %44;"
+            : "=r"(T[q][1]), "=r"(T[q][2]), "=r"(T[q][3]), "=r"(T[q][4]), "=r"(T[q][5]), "=r"(T[q][6]), "=r"(T[q][7]),
+              "=r"(T[q][8]), "=r"(T[q][9]), "=r"(T[q][10]), "=r"(T[q][11]), "=r"(T[q][12]), "=r"(T[q][13]),
+              "=r"(T[q][14]), "=r"(T[q][15])
+            : "r"(E[q][1]), "r"(E[q][2]), "r"(E[q][3]), "r"(E[q][4]), "r"(E[q][5]), "r"(E[q][6]), "r"(E[q][7]),
+              "r"(E[q][8]), "r"(E[q][9]), "r"(E[q][10]), "r"(E[q][11]), "r"(E[q][12]), "r"(E[q][13]), "r"(E[q][14]),
+              "r"(E[q][15]), "r"(O[q][0]), "r"(O[q][1]), "r"(O[q][2]), "r"(O[q][3]), "r"(O[q][4]), "r"(O[q][5]),
+              "r"(O[q][6]), "r"(O[q][7]), "r"(O[q][8]), "r"(O[q][9]), "r"(O[q][10]), "r"(O[q][11]), "r"(O[q][12]),
+              "r"(O[q][13]), "r"(O[q][14]));
+    }
+    uint32_t Ec[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) Ec[q] = 0;
+#pragma unroll
+    for (int rr = 0; rr < 4; rr++) {
+        const int bb = 2 * rr;
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            const uint32_t q0 = T[q][bb], q1 = T[q][bb + 1];
+            uint32_t w1, w2, w3;
+            asm("sub.cc.u32 %0, %3, %4;\n\t"
+                "subc.cc.u32 %1, %4, %3;\n\t"
+                "subc.u32 %2, %3, 0;"
+                : "=r"(w1), "=r"(w2), "=r"(w3)
+                : "r"(q1), "r"(q0));
+            if (rr > 0) {
+                asm("add.cc.u32 %0, %0, %2;\n\t"
+                    "addc.u32 %1, %1, 0;"
+                    : "+r"(w2), "+r"(w3)
+                    : "r"(Ec[q]));
+            }
+            asm("add.cc.u32 %0, %0, %8;\n\t"
+                "addc.cc.u32 %1, %1, %9;\n\t"
+                "addc.cc.u32 %2, %2, 0;\n\t"
+                "addc.cc.u32 %3, %3, %8;\n\t"
+                "addc.cc.u32 %4, %4, %10;\n\t"
+                "addc.cc.u32 %5, %5, %11;\n\t"
+                "addc.cc.u32 %6, %6, %12;\n\t"
+                "addc.u32 %7, 0, 0;"
+                : "+r"(T[q][bb + 3]), "+r"(T[q][bb + 4]), "+r"(T[q][bb + 5]), "+r"(T[q][bb + 6]), "+r"(T[q][bb + 7]),
+                  "+r"(T[q][bb + 8]), "+r"(T[q][bb + 9]), "=r"(Ec[q])
+                : "r"(q0), "r"(q1), "r"(w1), "r"(w2), "r"(w3));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+        uint32_t t[8], m;
+        asm("sub.cc.u32 %0, %9, 0xffffffff;\n\t"
+            "subc.cc.u32 %1, %10, 0xffffffff;\n\t"
+            "subc.cc.u32 %2, %11, 0xffffffff;\n\t"
+            "subc.cc.u32 %3, %12, 0;\n\t"
+            "subc.cc.u32 %4, %13, 0;\n\t"
+            "subc.cc.u32 %5, %14, 0;\n\t"
+            "subc.cc.u32 %6, %15, 1;\n\t"
+            "subc.cc.u32 %7, %16, 0xffffffff;\n\t"
+            "subc.u32 %8, %17, 0;"
+            : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7]), "=r"(m)
+            : "r"(T[q][8]), "r"(T[q][9]), "r"(T[q][10]), "r"(T[q][11]), "r"(T[q][12]), "r"(T[q][13]), "r"(T[q][14]),
+              "r"(T[q][15]), "r"(Ec[q]));
+#pragma unroll
+        for (int k = 0; k < 8; k++) r[q].v[k] = (T[q][8 + k] & m) | (t[k] & ~m);
+    }
 }
 
 }  // namespace pcmm
