@@ -397,6 +397,56 @@ PCMM_HD void s30_apply_de(s30 &d, s30 &e, const int32_t M[4], const s30 &P) {
     s30_reduce_1p5(e, P);
 }
 
+// (d, e) <- (u d + v e + md p, q d + r e + me p) / 2^30 for d, e in (-2p, p), without a reduction per
+// batch: md, me add p for each negative input (u [d < 0] + v [e < 0], ...) and are then corrected so that
+// the sums are multiples of 2^30 (p^-1 = -1 mod 2^30: md -= (md - cd) mod 2^30); with |u| + |v| and
+// |q| + |r| <= 2^30 (30 divsteps) the results stay in (-2p, p) (the bound of Bernstein-Yang's analysis as
+// used by libsecp256k1's modinv32).  Two 9-limb multiply-accumulate chains, no conditional passes.
+PCMM_HD void s30_update_de(s30 &d, s30 &e, const int32_t M[4], const s30 &P) {
+    const int32_t u = M[0], v = M[1], q = M[2], r = M[3];
+    const int32_t sd = d.v[8] >> 31, se = e.v[8] >> 31;
+    int32_t md = (u & sd) + (v & se);
+    int32_t me = (q & sd) + (r & se);
+    int64_t cd = (int64_t)u * d.v[0] + (int64_t)v * e.v[0];
+    int64_t ce = (int64_t)q * d.v[0] + (int64_t)r * e.v[0];
+    md -= (int32_t)(((uint32_t)md - (uint32_t)cd) & (uint32_t)kM30);
+    me -= (int32_t)(((uint32_t)me - (uint32_t)ce) & (uint32_t)kM30);
+    cd += (int64_t)P.v[0] * md;
+    ce += (int64_t)P.v[0] * me;
+    cd >>= 30;
+    ce >>= 30;
+#pragma unroll
+    for (int i = 1; i < 9; i++) {
+        cd += (int64_t)u * d.v[i] + (int64_t)v * e.v[i] + (int64_t)P.v[i] * md;
+        ce += (int64_t)q * d.v[i] + (int64_t)r * e.v[i] + (int64_t)P.v[i] * me;
+        d.v[i - 1] = (int32_t)(cd & kM30);
+        e.v[i - 1] = (int32_t)(ce & kM30);
+        cd >>= 30;
+        ce >>= 30;
+    }
+    d.v[8] = (int32_t)cd;
+    e.v[8] = (int32_t)ce;
+}
+
+// x^-1 = sign(f) d with d in (-2p, p) -> [0, p)
+PCMM_HD void s30_finish_inverse(fe &r, s30 d, const s30 &f, const s30 &P) {
+    if (s30_neg(f)) {
+        s30 z;
+        for (int i = 0; i < 9; i++) z.v[i] = 0;
+        s30_addmul(d, z, d, -1);                              // -d in (-p, 2p)
+    }
+    if (s30_neg(d)) s30_addmul(d, d, P, 1);
+    if (s30_neg(d)) s30_addmul(d, d, P, 1);
+    s30 y;
+    s30_addmul(y, d, P, -1);
+    if (!s30_neg(y)) d = y;                                   // [0, 2p) -> [0, p)
+    s30_to_words(r, d);
+}
+
+#ifndef PCMM_INV_LAZY_DE
+#define PCMM_INV_LAZY_DE 1      // 1: s30_update_de (no per-batch reduction of d, e), 0: s30_apply_de
+#endif
+
 // plain (non-Montgomery) x^-1 mod p for x in [0, p) (0 -> 0)
 PCMM_HD void fe_inv_plain_divsteps(fe &r, const fe &x) {
     fe pw;
@@ -418,9 +468,17 @@ PCMM_HD void fe_inv_plain_divsteps(fe &r, const fe &x) {
         int32_t M[4];
         zeta = divsteps30(zeta, (uint32_t)f.v[0] | ((uint32_t)f.v[1] << 30), (uint32_t)g.v[0] | ((uint32_t)g.v[1] << 30),
                           M);
+#if PCMM_INV_LAZY_DE
+        s30_update_de(d, e, M, P);
+#else
         s30_apply_de(d, e, M, P);
+#endif
         s30_apply_fg(f, g, M);
     }
+#if PCMM_INV_LAZY_DE
+    s30_finish_inverse(r, d, f, P);
+    return;
+#endif
     // f = +-1 (or p for x = 0, where d = 0): x^-1 = sign(f) d
     if (s30_neg(f)) {
         s30 z;
@@ -504,9 +562,17 @@ PCMM_HD void fe_inv_plain_divsteps_var(fe &r, const fe &x) {
         int32_t M[4];
         eta = divsteps30_var(eta, (uint32_t)f.v[0] | ((uint32_t)f.v[1] << 30), (uint32_t)g.v[0] | ((uint32_t)g.v[1] << 30),
                              M);
+#if PCMM_INV_LAZY_DE
+        s30_update_de(d, e, M, P);
+#else
         s30_apply_de(d, e, M, P);
+#endif
         s30_apply_fg(f, g, M);
     }
+#if PCMM_INV_LAZY_DE
+    s30_finish_inverse(r, d, f, P);
+    return;
+#endif
     if (s30_neg(f)) {
         s30 z;
         for (int i = 0; i < 9; i++) z.v[i] = 0;

@@ -33,6 +33,16 @@ int hfp_op(int op, const uint8_t *a_be, const uint8_t *b_be, uint8_t *out_be) {
     return 0;
 }
 
+// plain x^-1 mod p by the divsteps inversions (ct: constant-time half-delta, else variable-time)
+int hfp_inv_plain(int ct, const uint8_t *a_be, uint8_t *out_be) {
+    fe a, r;
+    fe_from_be_bytes(a, a_be);
+    if (ct) fe_inv_plain_divsteps(r, a);
+    else fe_inv_plain_divsteps_var(r, a);
+    fe_to_be_bytes(out_be, r);
+    return 0;
+}
+
 // raw Montgomery product of two (possibly unreduced < p) limb vectors
 int hfp_mont_mul_raw(const uint8_t *a_be, const uint8_t *b_be, uint8_t *out_be) {
     fe a, b, r;

@@ -86,7 +86,14 @@ def test_inversions_many_inputs():
         want = pow(a, -1, P)
         assert int.from_bytes(call(lib().hfp_op, 3, b32(a), b32(1)), "big") == want, hex(a)
         assert int.from_bytes(call(lib().hfp_op, 6, b32(a), b32(1)), "big") == want, hex(a)
+        # the plain-domain cores directly: constant-time (20 x 30 half-delta divsteps) and variable-time, both
+        # with the (d, e) update that keeps d, e in (-2p, p) without a per-batch reduction
+        want_plain = pow(a, -1, P)
+        assert int.from_bytes(call(lib().hfp_inv_plain, 1, b32(a)), "big") == want_plain, hex(a)
+        assert int.from_bytes(call(lib().hfp_inv_plain, 0, b32(a)), "big") == want_plain, hex(a)
     assert int.from_bytes(call(lib().hfp_op, 6, b32(0), b32(1)), "big") == 0
+    assert int.from_bytes(call(lib().hfp_inv_plain, 1, b32(0)), "big") == 0
+    assert int.from_bytes(call(lib().hfp_inv_plain, 0, b32(0)), "big") == 0
 
 
 def test_montgomery_raw_bound():
