@@ -469,15 +469,28 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         }
         LAUNCH("affine", s, launch_affine(tables, 2LL * nc * l * L.slots, atables, s, pc, nc, l, L.slots, iters, fast,
                                           status + 1));
-        const int ks = chunked ? std::min(choose_ksplit(m, nc, l, w), L.ksplit) : L.ksplit;   // <= partial slots
-        uint32_t *acc_out = (ks == 1 && !chunked) ? out : (uint32_t *)(ws + L.partial);
-        const int64_t split_stride = (ks == 1 && !chunked) ? 0 : 2LL * kPtWords * cnt;
-        if (w <= 4) {
-            LAUNCH("accum", s, launch_accum(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s));
-        } else {
-            LAUNCH("accum", s, launch_accum_global(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s));
+        // chunked: when one chunk's accumulation alone fills the GPU (>= 2 waves of CTAs), no split-k --
+        // each chunk adds straight into the running output (the accumulators start from it: 3 + 3
+        // products per output and chunk instead of a k_reduce pass with a complete addition per split)
+        int ks = L.ksplit;
+        if (chunked) {
+            const int rows = w <= 4 ? accum_rows(m) : 128;
+            const double ctas = (double)l * 2 * ((m + rows - 1) / rows);
+            const double resident =
+                (double)num_sms() * (w <= 4 ? accum_ctas_per_sm(L.slots, rows) : accum_global_ctas_per_sm());
+            ks = ctas >= 2 * resident ? 1 : std::min(choose_ksplit(m, nc, l, w), L.ksplit);   // <= partial slots
         }
-        if (ks > 1 || chunked) {
+        const bool direct = ks == 1;                  // the accumulate writes (and in chunks, adds into) `out`
+        uint32_t *acc_out = direct ? out : (uint32_t *)(ws + L.partial);
+        const int64_t split_stride = direct ? 0 : 2LL * kPtWords * cnt;
+        const int acc_in = direct && chunked && k0 > 0;
+        if (w <= 4) {
+            LAUNCH("accum", s, launch_accum(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in));
+        } else {
+            LAUNCH("accum", s,
+                   launch_accum_global(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in));
+        }
+        if (!direct) {
             uint32_t *partial = (uint32_t *)(ws + L.partial);
             LAUNCH("reduce", s, launch_reduce_splits(partial, ks, cnt, out, s, chunked && k0 > 0));
         }

@@ -114,11 +114,26 @@ __device__ __noinline__ void stage_chunk(const uint32_t *__restrict__ tables, co
     }
 }
 
+// The running output of earlier k-chunks (byte path, chunked, ksplit = 1): homogeneous (X : Y : Z) ->
+// the accumulator (Z = 0: the identity stays the initial value)
+__device__ __forceinline__ void acc_load_running(acc_t &acc, const uint32_t *ob, int64_t cnt, int64_t oi) {
+#ifdef __CUDA_ARCH__
+    pt o;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        o.X.v[q] = ob[(0 * 8 + q) * cnt + oi];
+        o.Y.v[q] = ob[(1 * 8 + q) * cnt + oi];
+        o.Z.v[q] = ob[(2 * 8 + q) * cnt + oi];
+    }
+    if (!fe_is_zero(o.Z)) acc_from_proj(acc, o);
+#endif
+}
+
 // R = rows per CTA (128, or 64 for m <= 64: twice the resident CTAs, no idle half-CTA)
 template <int S, int R>
 __global__ void __launch_bounds__(R, PCMM_ACCUM_MINB * (PCMM_ACC_ROWS / R))
     k_accum(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int ksplit,
-            uint32_t *__restrict__ out, int64_t split_stride) {
+            uint32_t *__restrict__ out, int64_t split_stride, int acc_in) {
     constexpr int ROWS = AccumCfg<S, R>::kRows, KCH = AccumCfg<S, R>::kChunk;
     constexpr int EW = AccumCfg<S, R>::kEW, TWS = AccumCfg<S, R>::kTWs;
     extern __shared__ uint4 smem4[];
@@ -136,6 +151,7 @@ __global__ void __launch_bounds__(R, PCMM_ACCUM_MINB * (PCMM_ACC_ROWS / R))
     PCMM_DCHECK(blockDim.x == ROWS && s < ksplit && c < 2);
     acc_t acc;
     acc_init(acc);
+    if (acc_in && i < m) acc_load_running(acc, out + (int64_t)c * kPtWords * m * l, (int64_t)m * l, (int64_t)i * l + j);
     for (int k0 = kb; k0 < ke; k0 += KCH) {
         const int kc = min(KCH, ke - k0);
         __syncthreads();
@@ -208,7 +224,7 @@ constexpr int kRowsG = 128;
 
 __global__ void __launch_bounds__(kRowsG, 3)
     k_accum_g(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int S,
-              int ksplit, uint32_t *__restrict__ out, int64_t split_stride) {
+              int ksplit, uint32_t *__restrict__ out, int64_t split_stride, int acc_in) {
     int b = blockIdx.x;
     const int j = b % l; b /= l;
     const int c = b & 1; b >>= 1;
@@ -222,6 +238,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
     const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kAffWords;
     acc_t acc;
     acc_init(acc);
+    if (acc_in) acc_load_running(acc, out + (int64_t)c * kPtWords * m * l, (int64_t)m * l, (int64_t)i * l + j);
     int k = kb;
     while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
     if (k < ke) {
@@ -320,10 +337,10 @@ int accum_global_ctas_per_sm() {
 }
 
 cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
-                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in) {
     const int rowblocks = (m + kRowsG - 1) / kRowsG;
     const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
-    k_accum_g<<<grid, kRowsG, 0, s>>>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split);
+    k_accum_g<<<grid, kRowsG, 0, s>>>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, acc_in);
     return cudaGetLastError();
 }
 
@@ -411,34 +428,34 @@ int accum_chunk(int slots) {
 
 template <int S, int R>
 static cudaError_t launch_accum_s(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int ksplit,
-                                  uint32_t *out, int64_t stride, cudaStream_t s) {
+                                  uint32_t *out, int64_t stride, cudaStream_t s, int acc_in) {
     const int rowblocks = (m + R - 1) / R;
     const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
     cudaError_t err =
         cudaFuncSetAttribute(k_accum<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AccumCfg<S, R>::kSmem);
     if (err) return err;
-    k_accum<S, R><<<grid, R, AccumCfg<S, R>::kSmem, s>>>(tables, rank, m, n, l, ksplit, out, stride);
+    k_accum<S, R><<<grid, R, AccumCfg<S, R>::kSmem, s>>>(tables, rank, m, n, l, ksplit, out, stride, acc_in);
     return cudaGetLastError();
 }
 
 template <int R>
 static cudaError_t launch_accum_r(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
-                                  int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+                                  int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in) {
     switch (slots) {
-        case 2: return launch_accum_s<2, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        case 4: return launch_accum_s<4, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        case 8: return launch_accum_s<8, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
-        default: return launch_accum_s<16, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s);
+        case 2: return launch_accum_s<2, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s, acc_in);
+        case 4: return launch_accum_s<4, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s, acc_in);
+        case 8: return launch_accum_s<8, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s, acc_in);
+        default: return launch_accum_s<16, R>(tables, rank, m, n, l, ksplit, out, out_stride_split, s, acc_in);
     }
 }
 
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
-                         uint32_t *out, int64_t out_stride_split, cudaStream_t s) {
+                         uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in) {
 #if PCMM_ACC_ROWS == 128
     if (accum_rows(m) == 64)
-        return launch_accum_r<64>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s);
+        return launch_accum_r<64>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s, acc_in);
 #endif
-    return launch_accum_r<PCMM_ACC_ROWS>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s);
+    return launch_accum_r<PCMM_ACC_ROWS>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, s, acc_in);
 }
 
 cudaError_t launch_bench_fp_mul(int variant, int blocks, int threads, int iters, uint32_t *out, cudaStream_t s) {

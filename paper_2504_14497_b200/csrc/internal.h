@@ -65,11 +65,12 @@ int tables_coz_mode();   // PCMM_TABLES_COZ: 0 off, 1 auto (default), 2 always (
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
 // kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
 inline int max_upper(int w) { return w <= 4 ? 8 : 32; }
+// acc_in (ksplit = 1 only): start each accumulator from the running output in `out` (k-chunked byte path)
 cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
-                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s);
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in = 0);
 int accum_global_ctas_per_sm();
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
-                         uint32_t *out, int64_t out_stride_split, cudaStream_t s);
+                         uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in = 0);
 // out = sum of the ksplit partial sums (+ out itself when accumulate: the byte path's k-chunks)
 cudaError_t launch_reduce_splits(const uint32_t *partial, int ksplit, int64_t count, uint32_t *out, cudaStream_t s,
                                  bool accumulate = false);

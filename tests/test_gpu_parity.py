@@ -808,6 +808,22 @@ def test_byte_path_k_chunks_forced():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_c256_chunked_direct_every_output():
+    # 256^3 w = 4 with a 100 MB table budget: k-chunks large enough that each chunk's accumulation fills the
+    # GPU, so k_accum adds each chunk straight into the running output (no split-k, no k_reduce); every
+    # output against the oracle
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_BYTE_BUDGET_MB="100")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_full_size_cussen_every_output and c256"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout, r.stdout[-500:]
+
+
 def test_c512_w8_chunked_sampled():
     # 512^3 at w = 8 (tables of all k would take ~21 GB): the default 2 GiB budget chunks k;
     # sampled outputs vs the Eq. 5 closed form
