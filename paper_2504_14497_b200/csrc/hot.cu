@@ -28,6 +28,9 @@ __device__ __forceinline__ void soa_store_hot(uint32_t *base, int64_t stride, in
 #ifndef PCMM_ACCUM_CHUNK_SLOTS
 #define PCMM_ACCUM_CHUNK_SLOTS 512  // table slots staged per chunk: k-chunk = this / 2^w (32 at w = 4)
 #endif
+#ifndef PCMM_ACC_UNROLL2
+#define PCMM_ACC_UNROLL2 0      // 1: two pipelined steps per loop trip, entry registers alternating roles
+#endif
 #ifndef PCMM_ACC_LAZY
 // 1: almost-reduced values in the pipelined step (jac.cuh xyzz_add_aff_pipe_lz: no final conditional
 // subtraction in the products, lazy sums / differences).  Measured 8 % slower at 256^3 (3.95 vs
@@ -165,6 +168,26 @@ __global__ void __launch_bounds__(R, PCMM_ACCUM_MINB * (PCMM_ACC_ROWS / R))
             fe x2, y2, U2;
             bool have_u2 = false;
             ld_entry<EW>(x2, y2, tsm + kk * TWS + rsm[kk * ROWS + tid] * EW);
+#if PCMM_ACC_UNROLL2
+            // two steps per trip with the entry registers alternating roles (no x2 = xn copies)
+            fe xn, yn;
+            while (true) {
+                int kn = kk + 1;
+                while (kn < kc && rsm[kn * ROWS + tid] == 0) kn++;
+                bool more = kn < kc;
+                ld_entry<EW>(xn, yn, tsm + (more ? kn * TWS + rsm[kn * ROWS + tid] * EW : kk * TWS + rsm[kk * ROWS + tid] * EW));
+                xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);
+                if (!more) break;
+                kk = kn;
+                kn = kk + 1;
+                while (kn < kc && rsm[kn * ROWS + tid] == 0) kn++;
+                more = kn < kc;
+                ld_entry<EW>(x2, y2, tsm + (more ? kn * TWS + rsm[kn * ROWS + tid] * EW : kk * TWS + rsm[kk * ROWS + tid] * EW));
+                xyzz_add_aff_pipe(acc, xn, yn, U2, have_u2, x2);
+                if (!more) break;
+                kk = kn;
+            }
+#else
             while (true) {
                 int kn = kk + 1;
                 while (kn < kc && rsm[kn * ROWS + tid] == 0) kn++;
@@ -182,6 +205,7 @@ __global__ void __launch_bounds__(R, PCMM_ACCUM_MINB * (PCMM_ACC_ROWS / R))
                 y2 = yn;
                 kk = kn;
             }
+#endif
         }
 #else
         while (kk < kc) {
