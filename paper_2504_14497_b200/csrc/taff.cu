@@ -100,6 +100,9 @@ __device__ __forceinline__ fe warp_inverse(const fe &a, const fe &one) {
 #ifndef PCMM_TCOZ_MINB
 #define PCMM_TCOZ_MINB 4
 #endif
+#ifndef PCMM_TCOZ_PREFETCH
+#define PCMM_TCOZ_PREFETCH 1    // 1 (default; 256^3 tables 0.406 -> 0.376 ms): backward pass loads the next parked entry before the current entry's products
+#endif
 
 // Builds the chain of one table (c, k, j) and returns whether it has entries
 // to convert (n1 >= 2 in a consecutive column, component not the identity),
@@ -225,6 +228,33 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
         fe_mul(zinv, inv, pre);                                         // 1 / Z_{n1}
         fe_mul(inv, inv, Zf);
         // backward: x = X / Z^2, y = Y / Z^3, then 1 / Z_{u-1} = lambda_{u-1} / Z_u
+#if PCMM_TCOZ_PREFETCH
+        // the next entry's parked (X, Y, lambda) are loaded before this entry's products (the loads'
+        // L2 / HBM latency overlaps the arithmetic instead of stalling the chain)
+        fe X, Y, lam;
+        ld_xy(X, Y, pblk + pl.n[0] * kPtWords);
+        ld_x(lam, pblk + pl.n[0] * kPtWords + 16);
+        for (int u = pl.n[0]; u >= 2; u--) {
+            fe Xn, Yn, lamn;
+            if (u >= 3) {
+                const uint32_t *qn = pblk + (u - 1) * kPtWords;
+                ld_xy(Xn, Yn, qn);
+                ld_x(lamn, qn + 16);
+            }
+            fe zi2, zi3, x, y;
+            fe_sqr(zi2, zinv);
+            fe_mul(x, X, zi2);
+            fe_mul(zi3, zi2, zinv);
+            fe_mul(y, Y, zi3);
+            st_xy(ablk + u * kAffWords, x, y);
+            if (u >= 3) {
+                fe_mul(zinv, zinv, lam);
+                X = Xn;
+                Y = Yn;
+                lam = lamn;
+            }
+        }
+#else
         for (int u = pl.n[0]; u >= 2; u--) {
             const uint32_t *q = pblk + u * kPtWords;
             fe X, Y, zi2, zi3, x, y;
@@ -240,6 +270,7 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
                 fe_mul(zinv, zinv, lam);
             }
         }
+#endif
 #if PCMM_TCOZ_DISCARD
         // the parked (X, Y, lambda) and (prefix, Z) are dead: drop their L2 lines without writing them back
         if ((S * kPtWords * 4) % 128 == 0) {
