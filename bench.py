@@ -34,9 +34,13 @@ import synth  # noqa: E402
 
 METRIC = "encrypted output entries/s and EC point-adds/s; % of INT32-IMAD fp_mul roofline"
 UNIT = "entries/s"
-# Roofline denominator: 32x32->64 products / clk / SM on the
-# IMAD pipe (IMAD.WIDE.U32 issues at half the IMAD rate; K11 probe, profiles/k11_imad.txt)
-P_PROD = 32.0
+# Roofline denominator (DESIGN.md §6 "Machine model"): 32x32->64 products / clk / SM, the best measured
+# rate of the product instruction in the form the field product issues it (carry chains of
+# IMAD.WIDE.U32 + IMAD.WIDE.U32.X): 52.2 at 48-64 warps per SM (tools/k12_chain_probe.cu,
+# profiles/r02_k12_chain_probe_nc2.txt).  Round 1 used 32.0 from K11's mul.wide probe
+# (profiles/r01_k11_imad.txt), whose operands came from one register pair; K12 supersedes it.
+P_PROD = 52.2
+P_PROD_K11 = 32.0
 LIMB_PRODUCTS_PER_FPMUL = 64.0
 # Algorithmic work numerator F of SURVEY.md §8(d) (fixed per input, not per implementation):
 #   F = 14 (useful complete adds) + 13 (doublings) + 6 (normalised points)
@@ -471,14 +475,19 @@ class Problem:
                 "bound": "alu", "kernel": "k_accum (+k_reduce)", "achieved": ach, "peak": g.peak,
                 "unit": "G fp_mul/s", "frac": ach / g.peak, "traffic": traffic, "traffic_source": tsrc,
                 "frac_executed_products": ex / g.peak,
+                "frac_vs_r01_peak": ach / (g.peak * P_PROD_K11 / P_PROD),
                 "algorithmic": f"SURVEY.md §8(d): 14 fp_mul per useful complete addition x {W['acc_adds']} "
                                f"useful accumulate additions (a_ik != 0) over the kernel time {t_acc:.4f} ms "
                                f"(library CUDA events on the launching stream)",
                 "executed": f"frac_executed_products: the products the kernel issues, {EXEC_PER_ACC_ADD} "
                             f"fp_mul-equivalents per XYZZ + affine mixed addition (8M + 2S, squares at 36/64)",
-                "peak_note": f"{g.nsm} SM x {P_PROD:.0f} 32x32->64 products/clk/SM x {g.f_max / 1e9:.3f} GHz "
-                             f"(sm_max) / 64 products per fp_mul; IMAD.WIDE half-rate measured by "
-                             f"tools/k11_imad_probe.cu (profiles/r01_k11_imad.txt)"}
+                "peak_note": f"{g.nsm} SM x {P_PROD:.1f} 32x32->64 products/clk/SM x {g.f_max / 1e9:.3f} GHz "
+                             f"(sm_max) / 64 products per fp_mul; {P_PROD:.1f} = IMAD.WIDE.U32(.X) carry chains "
+                             f"alone at 48-64 warps per SM (tools/k12_chain_probe.cu, "
+                             f"profiles/r02_k12_chain_probe_nc2.txt); the kernel's own instruction mix "
+                             f"(1.8 ALU instructions per IMAD.WIDE, issue costs add: DESIGN.md §6) bounds it "
+                             f"at ~0.47 of this peak at full issue efficiency; frac_vs_r01_peak is against "
+                             f"round 1's {P_PROD_K11:.0f}/clk/SM (K11's mul.wide probe, superseded)"}
         if with_school and self.path == P.CUSSEN:
             ws_sb = P.alloc_workspace(cfg.m, cfg.n, cfg.l, cfg.w, P.SCHOOLBOOK, g.dev, wide=self.wide)
 

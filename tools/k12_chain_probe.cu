@@ -62,10 +62,13 @@
                  : "r"(f))
 
 constexpr int ITERS = 512;
-constexpr int NC = 4;          // accumulator sets per thread
+#ifndef K12_NC
+#define K12_NC 4
+#endif
+constexpr int NC = K12_NC;     // accumulator sets per thread
 
-template <int MODE>
-__global__ void __launch_bounds__(256, 2) probe(uint32_t *out, long long *cyc, uint32_t seed) {
+template <int MODE, int MB = 2>
+__global__ void __launch_bounds__(256, MB) probe(uint32_t *out, long long *cyc, uint32_t seed) {
     uint32_t d[NC][9], e[NC][6];
     uint64_t w[NC][4];
     const uint32_t t = threadIdx.x + seed;
@@ -134,20 +137,20 @@ __global__ void __launch_bounds__(256, 2) probe(uint32_t *out, long long *cyc, u
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int MODE>
+template <int MODE, int MB = 2>
 static void run(const char *name, double wide_per_set, double instr_per_set, int nsm, uint32_t *d_out, long long *d_cyc) {
-    const int blocks = nsm * 2;
-    probe<MODE><<<blocks, 256>>>(d_out, d_cyc, 1);
+    const int blocks = nsm * MB;
+    probe<MODE, MB><<<blocks, 256>>>(d_out, d_cyc, 1);
     cudaDeviceSynchronize();
-    probe<MODE><<<blocks, 256>>>(d_out, d_cyc, 2);
+    probe<MODE, MB><<<blocks, 256>>>(d_out, d_cyc, 2);
     cudaDeviceSynchronize();
     static long long h[4096];
     cudaMemcpy(h, d_cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
     double mean = 0;
     for (int i = 0; i < blocks; i++) mean += h[i];
     mean /= blocks;
-    // 2 CTAs of 256 threads per SM run concurrently: 512 threads per SM over `mean` cycles
-    const double sets = 512.0 * ITERS * NC;
+    // MB CTAs of 256 threads per SM run concurrently over `mean` cycles
+    const double sets = 256.0 * MB * ITERS * NC;
     printf("%-44s IMAD.WIDE/clk/SM = %6.2f   warp-instr/clk/SMSP = %.3f   (cycles %.0f)  %s\n", name,
            sets * wide_per_set / mean, sets * instr_per_set / mean / 128.0, mean, cudaGetErrorString(cudaGetLastError()));
 }
@@ -158,8 +161,8 @@ int main() {
     const int nsm = p.multiProcessorCount;
     uint32_t *d_out;
     long long *d_cyc;
-    cudaMalloc(&d_out, sizeof(uint32_t) * nsm * 2 * 256);
-    cudaMalloc(&d_cyc, sizeof(long long) * nsm * 2);
+    cudaMalloc(&d_out, sizeof(uint32_t) * nsm * 8 * 256);
+    cudaMalloc(&d_cyc, sizeof(long long) * nsm * 8);
     run<0>("0 IMAD.WIDE R,R,R,R (64-bit addend)", 4, 4, nsm, d_out, d_cyc);
     run<1>("1 chain4 + addc (fe_prod_eo row)", 4, 5, nsm, d_out, d_cyc);
     run<2>("2 chain4 (IMAD.WIDE + 3 IMAD.WIDE.X)", 4, 4, nsm, d_out, d_cyc);
@@ -171,5 +174,15 @@ int main() {
     run<8>("8 6 independent IADD alone", 0, 6, nsm, d_out, d_cyc);
     run<9>("9 6 LOP3 alone", 0, 6, nsm, d_out, d_cyc);
     run<10>("10 4 IMAD.WIDE RZ + 4 LOP3", 4, 8, nsm, d_out, d_cyc);
+    run<2, 4>("2 chain4, 32 warps/SM", 4, 4, nsm, d_out, d_cyc);
+    run<1, 4>("1 chain4 + addc, 32 warps/SM", 4, 5, nsm, d_out, d_cyc);
+    run<3, 4>("3 chain4 + addc + 6 IADD3.X, 32 warps/SM", 4, 11, nsm, d_out, d_cyc);
+    run<4, 4>("4 6 IADD3(.X) chain alone, 32 warps/SM", 0, 6, nsm, d_out, d_cyc);
+    run<2, 1>("2 chain4, 8 warps/SM", 4, 4, nsm, d_out, d_cyc);
+#if K12_NC <= 2
+    run<2, 6>("2 chain4, 48 warps/SM", 4, 4, nsm, d_out, d_cyc);
+    run<2, 8>("2 chain4, 64 warps/SM", 4, 4, nsm, d_out, d_cyc);
+    run<1, 8>("1 chain4 + addc, 64 warps/SM", 4, 5, nsm, d_out, d_cyc);
+#endif
     return 0;
 }
