@@ -455,7 +455,8 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         // (64^3: the general kernel runs anyway for the rest and the extra launch costs more)
         // (k_tables_coz, default: the same columns, tables and affine conversion in one kernel; k_affine skips them)
         const int amode = tables_coz_mode();
-        const int aff = !is_signed && iters >= 2 && (amode == 2 || (amode == 1 && 2LL * nc * l >= 65536));
+        // (signed A: columns whose magnitudes are {1..M}, R10b; the others take k_tables + k_affine)
+        const int aff = iters >= 2 && (amode == 2 || (amode == 1 && 2LL * nc * l >= 65536));
         const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * nc * l >= 65536);
         LAUNCH("tables", s, launch_tables(bc, pc, nc, l, iters, L.slots, L.maxup, is_signed, tables,
                                           (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1),

@@ -12,10 +12,16 @@ namespace pcmm {
 // ptr[w-1][e] = index in a^(w+1) of element e of the differenced level-w vector
 // (the tracking pointer used by the un-sort / re-insert of level w+1 -> w).
 constexpr int kPlanCap = 256;         // |a^(1)| <= 255 for int8 plaintexts
+// coz > 0: the column's table is the chain P, 2P, ..., coz P (k_tables_coz): unsigned columns with
+// a^(1) = {1..coz} (levels 2..N = {1}), or, sgn = 1, signed columns whose magnitudes are {1..coz}
+// (each in either sign; R10b: the entry of -v is the negated entry of v).  bm1 = the level-1
+// presence bitmap (bit v + 128), from which k_tables_coz finds the slot of +-v.
 struct ColPlan {
     int16_t n[4];
+    int16_t coz, sgn;
     int16_t sN[kPlanCap];
     uint8_t ptr[3][kPlanCap];
+    uint32_t bm1[12];
 };
 constexpr int kPtWords = 24;          // X, Y, Z x 8 limbs
 constexpr int kAffWords = 16;         // affine table entry: x, y x 8 limbs (identity: x = all ones)

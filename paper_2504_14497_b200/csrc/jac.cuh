@@ -192,6 +192,24 @@ __device__ __forceinline__ void jac_dbl(jacc &A) {
 // product fewer than the Jacobian step above (which also has to form Z^3 and
 // Z3 = Z1 H).  Same exceptional cases as jac_add_aff (identity, P = 0), which
 // take the complete RCB16 path on homogeneous images.
+#ifndef PCMM_ACC_PERM
+#define PCMM_ACC_PERM 0         // 1: product order / operand order of the pipelined step from PCMM_G1, _G2, _G3, _SWAPM
+#endif
+#ifndef PCMM_G1
+#define PCMM_G1 12
+#endif
+#ifndef PCMM_G2
+#define PCMM_G2 1234
+#endif
+#ifndef PCMM_G3
+#define PCMM_G3 1234
+#endif
+#ifndef PCMM_SWAPM
+#define PCMM_SWAPM 0
+#endif
+#ifndef PCMM_ACC_LZ3
+#define PCMM_ACC_LZ3 0          // 1: PP, ZZ3, ZZZ3 of the pipelined step without the final conditional subtraction
+#endif
 struct xyzz {
     fe X, Y, ZZ, ZZZ;
     uint32_t inf;                 // 1 while the accumulator is the identity
@@ -277,8 +295,16 @@ __device__ __forceinline__ void xyzz_to_proj(pt &o, const xyzz &A) {
     if (A.inf) {
         pt_identity(o);
     } else {
+#if PCMM_ACC_LZ3
+        fe zz, zzz;                               // ZZ, ZZZ may be in [p, 2^256) (xyzz_add_aff_pipe)
+        fe_cond_sub_p(zz, A.ZZ, 0);
+        fe_cond_sub_p(zzz, A.ZZZ, 0);
+        mul2(o.X, A.X, zzz, o.Y, A.Y, zz);
+        o.Z = fe_mul_call(zz, zzz);
+#else
         mul2(o.X, A.X, A.ZZZ, o.Y, A.Y, A.ZZ);
         o.Z = fe_mul_call(A.ZZ, A.ZZZ);
+#endif
     }
 #endif
 }
@@ -363,6 +389,64 @@ __device__ __forceinline__ void xyzz_add_aff_pipe(xyzz &A, const fe &x2, const f
         have_u2 = false;
         return;
     }
+#if PCMM_ACC_LZ3
+    // PP, ZZ3 and ZZZ3 feed only products: they skip the final conditional subtraction (values in
+    // [0, 2^256)); every product with one canonical operand is canonical again (fp_fast.cuh).
+    fe2 sp;
+    fe_mul_fast(sp.x, y2, A.ZZZ);                            // S2 = y2 ZZZ
+    fe_sqr_lz(sp.y, P);                                      // PP = P^2 (lazy)
+    fe_sub(R, sp.x, A.Y);
+    fe4 t;
+    fe_sqr_fast(t.x, R);                                     // R^2
+    fe_mul_fast(t.y, P, sp.y);                               // PPP
+    fe_mul_fast(t.z, A.X, sp.y);                             // Q = X1 PP
+    fe_mul_lz(t.w, A.ZZ, sp.y);                              // ZZ3 (lazy)
+    fe X3, Q2, D;
+    fe_add(Q2, t.z, t.z);
+    fe_sub(X3, t.x, t.y);
+    fe_sub(X3, X3, Q2);                                     // X3 = R^2 - PPP - 2Q
+    fe_sub(D, t.z, X3);
+    fe4 u;
+    fe_mul_fast(u.x, R, D);                                  // R (Q - X3)
+    fe_mul_fast(u.y, A.Y, t.y);                              // Y1 PPP
+    fe_mul_lz(u.z, A.ZZZ, t.y);                              // ZZZ3 (lazy)
+    fe_mul_fast(u.w, xn, t.w);                               // U2'
+#elif PCMM_ACC_PERM
+    // the same ten products in a source order chosen by macros (schedule search, tools/perm_search.sh):
+    // PCMM_G1 / PCMM_G2 / PCMM_G3 = the order of each group's products as decimal digits,
+    // PCMM_SWAPM = bit mask swapping the operands of the eight general products
+    fe2 sp;
+#pragma unroll
+    for (int st = 0; st < 2; st++) {
+        const int d = st == 0 ? (PCMM_G1 / 10) % 10 : PCMM_G1 % 10;
+        if (d == 1) { if (PCMM_SWAPM & 1) fe_mul_fast(sp.x, A.ZZZ, y2); else fe_mul_fast(sp.x, y2, A.ZZZ); }
+        if (d == 2) fe_sqr_fast(sp.y, P);
+    }
+    fe_sub(R, sp.x, A.Y);
+    fe4 t;
+#pragma unroll
+    for (int st = 0; st < 4; st++) {
+        const int d = st == 0 ? (PCMM_G2 / 1000) % 10 : st == 1 ? (PCMM_G2 / 100) % 10 : st == 2 ? (PCMM_G2 / 10) % 10 : PCMM_G2 % 10;
+        if (d == 1) fe_sqr_fast(t.x, R);
+        if (d == 2) { if (PCMM_SWAPM & 2) fe_mul_fast(t.y, sp.y, P); else fe_mul_fast(t.y, P, sp.y); }
+        if (d == 3) { if (PCMM_SWAPM & 4) fe_mul_fast(t.z, sp.y, A.X); else fe_mul_fast(t.z, A.X, sp.y); }
+        if (d == 4) { if (PCMM_SWAPM & 8) fe_mul_fast(t.w, sp.y, A.ZZ); else fe_mul_fast(t.w, A.ZZ, sp.y); }
+    }
+    fe X3, Q2, D;
+    fe_add(Q2, t.z, t.z);
+    fe_sub(X3, t.x, t.y);
+    fe_sub(X3, X3, Q2);                                     // X3 = R^2 - PPP - 2Q
+    fe_sub(D, t.z, X3);
+    fe4 u;
+#pragma unroll
+    for (int st = 0; st < 4; st++) {
+        const int d = st == 0 ? (PCMM_G3 / 1000) % 10 : st == 1 ? (PCMM_G3 / 100) % 10 : st == 2 ? (PCMM_G3 / 10) % 10 : PCMM_G3 % 10;
+        if (d == 1) { if (PCMM_SWAPM & 16) fe_mul_fast(u.x, D, R); else fe_mul_fast(u.x, R, D); }
+        if (d == 2) { if (PCMM_SWAPM & 32) fe_mul_fast(u.y, t.y, A.Y); else fe_mul_fast(u.y, A.Y, t.y); }
+        if (d == 3) { if (PCMM_SWAPM & 64) fe_mul_fast(u.z, t.y, A.ZZZ); else fe_mul_fast(u.z, A.ZZZ, t.y); }
+        if (d == 4) { if (PCMM_SWAPM & 128) fe_mul_fast(u.w, t.w, xn); else fe_mul_fast(u.w, xn, t.w); }
+    }
+#else
     const fe2 sp = fe_mulsqr_hot(y2, A.ZZZ, P);              // S2 = y2 ZZZ, PP = P^2
     fe_sub(R, sp.x, A.Y);
     const fe4 t = fe_sqr_mul3_hot(R, P, sp.y, A.X, sp.y, A.ZZ, sp.y);   // R^2, PPP, Q = X1 PP, ZZ3
@@ -372,6 +456,7 @@ __device__ __forceinline__ void xyzz_add_aff_pipe(xyzz &A, const fe &x2, const f
     fe_sub(X3, X3, Q2);                                     // X3 = R^2 - PPP - 2Q
     fe_sub(D, t.z, X3);
     const fe4 u = fe_mul4_hot(R, D, A.Y, t.y, A.ZZZ, t.y, xn, t.w);   // R (Q - X3), Y1 PPP, ZZZ3, U2'
+#endif
     fe_sub(A.Y, u.x, u.y);
     A.X = X3;
     A.ZZ = t.w;

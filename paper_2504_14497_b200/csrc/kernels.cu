@@ -90,6 +90,27 @@ __global__ void k_plan(const int8_t *__restrict__ A, int m, int n, int w, int is
     for (int q = 0; q < 12; q++)                                          // level 1 (R1), ascending
         for (uint32_t x = bm[q]; x; x &= x - 1u) s[ns++] = (int16_t)(32 * q + __ffs(x) - 1 - kBmOff);
     for (int q = 0; q < 4; q++) P->n[q] = 0;
+    for (int q = 0; q < 12; q++) P->bm1[q] = bm[q];
+    // chain columns (k_tables_coz): unsigned {1..ns}; signed with every magnitude 1..M present in some sign
+    int coz = 0, sgn = 0;
+    if (N >= 2 && ns >= 1) {
+        if (!is_signed) {
+            if (s[ns - 1] == ns) coz = ns;
+        } else {
+            const int M = max(abs((int)s[0]), abs((int)s[ns - 1]));
+            bool ok = true;
+            for (int u = 1; u <= M; u++) {
+                const int bp = kBmOff + u, bn = kBmOff - u;
+                if (!(((bm[bp >> 5] >> (bp & 31)) | (bm[bn >> 5] >> (bn & 31))) & 1u)) ok = false;
+            }
+            if (ok) {
+                coz = M;
+                sgn = 1;
+            }
+        }
+    }
+    P->coz = (int16_t)coz;
+    P->sgn = (int16_t)sgn;
     for (int lev = 1; lev <= N; lev++) {
         if (lev > 1) {
             // level lev: sorted distinct values of the differenced level lev-1 (v, ns entries)

@@ -8,7 +8,8 @@ namespace pcmm {
 // Column k's tables are built by k_tables_fast (below) when its level-1 set is
 // {1, ..., n1}; k_tables / k_affine then skip it.  (k_affine: plans == nullptr, no skipping)
 __device__ __forceinline__ bool col_consecutive(const ColPlan &pl, int N) {
-    return N >= 2 && pl.n[0] >= 1 && pl.n[1] == 1 && pl.sN[0] == 1;
+    (void)N;
+    return pl.coz > 0;          // set by k_plan (N >= 2; unsigned {1..n1} or signed magnitudes {1..M})
 }
 
 #ifndef PCMM_TFAST_PROJ

@@ -104,10 +104,38 @@ __device__ __forceinline__ fe warp_inverse(const fe &a, const fe &one) {
 #define PCMM_TCOZ_PREFETCH 1    // 1 (default; 256^3 tables 0.406 -> 0.376 ms): backward pass loads the next parked entry before the current entry's products
 #endif
 
+// Slot of the value v of column pl (1 + the number of level-1 values below v), or -1 if v does not
+// occur.  Unsigned chain columns: the values are {1..coz}, slot v = v.
+__device__ __forceinline__ int coz_slot(const ColPlan &pl, int v) {
+    if (!pl.sgn) return v;
+    const int b = v + 128;
+    if (!((pl.bm1[b >> 5] >> (b & 31)) & 1u)) return -1;
+    int r = 0;
+    for (int q = 0; q < (b >> 5); q++) r += __popc(pl.bm1[q]);
+    return 1 + r + __popc(pl.bm1[b >> 5] & ((1u << (b & 31)) - 1u));
+}
+
+// (x, y) -> the slots of +u and -u ((x, -y): DESIGN.md R10b) that the column has
+__device__ __forceinline__ void coz_store(const ColPlan &pl, uint32_t *ablk, int u, const fe &x, const fe &y, int S) {
+    const int sp = coz_slot(pl, u);
+    PCMM_DCHECK(sp < S);
+    if (sp >= 1) st_xy(ablk + sp * kAffWords, x, y);
+    if (pl.sgn) {
+        const int sn = coz_slot(pl, -u);
+        PCMM_DCHECK(sn < S);
+        if (sn >= 1) {
+            fe zero, ny;
+            fe_zero(zero);
+            fe_sub(ny, zero, y);
+            st_xy(ablk + sn * kAffWords, x, ny);
+        }
+    }
+}
+
 // Builds the chain of one table (c, k, j) and returns whether it has entries
-// to convert (n1 >= 2 in a consecutive column, component not the identity),
-// with the Z of its last entry.  Writes the affine slots 0, 1 and > n1 and
-// parks (X, Y, lambda) of entries 2..n1 in their projective slots.  (Running
+// to convert (chain length >= 2, component not the identity), with the Z of its
+// last entry.  Writes the affine slots 0, +-1 and the unused ones and parks
+// (X, Y, lambda) of the multiples 2..n1 in projective slots 2..n1.  (Running
 // the two components' chains in lockstep in one thread halves the thread count
 // and measured slower: 256^3 0.47 vs 0.39 ms.)
 __device__ __forceinline__ bool coz_chain(const uint32_t *__restrict__ bsoa, const ColPlan *__restrict__ plans,
@@ -118,20 +146,21 @@ __device__ __forceinline__ bool coz_chain(const uint32_t *__restrict__ bsoa, con
     const int c = (int)(t / ((int64_t)l * n));
     const ColPlan &pl = plans[k];
     if (!col_consecutive(pl, N)) return false;
-    const int n1 = pl.n[0];
-    PCMM_DCHECK(n1 < S && t < 2LL * n * l);
+    const int n1 = pl.coz;                                              // chain length (multiples 1..n1)
+    const int used = pl.n[0];                                           // slots 1..used hold entries
+    PCMM_DCHECK(n1 < S && used < S && t < 2LL * n * l);
     uint32_t *ablk = atab + t * (int64_t)(kAffWords * S);              // table index (c n + k) l + j = t
     uint32_t *pblk = ptab + t * (int64_t)(kPtWords * S);
     st_aff_inf(ablk);                                                   // slot 0 = the identity
-    for (int u = n1 + 1; u < S; u++) st_aff_inf(ablk + u * kAffWords);
+    for (int u = used + 1; u < S; u++) st_aff_inf(ablk + u * kAffWords);
     const int64_t cnt = (int64_t)n * l;
     pt P;
     soa_load(P, bsoa + (int64_t)c * kPtWords * cnt, cnt, (int64_t)k * l + j);
     if (pt_is_identity(P)) {                                            // every multiple is the identity
-        for (int u = 1; u <= n1; u++) st_aff_inf(ablk + u * kAffWords);
+        for (int u = 1; u <= used; u++) st_aff_inf(ablk + u * kAffWords);
         return false;
     }
-    st_xy(ablk + kAffWords, P.X, P.Y);                                  // T[1] = P (Z = 1 after k_import)
+    coz_store(pl, ablk, 1, P.X, P.Y, S);                                // T[+-1] = +-P (Z = 1 after k_import)
     if (n1 < 2) return false;
     // DBLU: 2P on Z = 2y, and P on the same Z: (4 x y^2, 8 y^4)
     fe B, E, L, Sx, M, X2, Y2, t0;
@@ -201,6 +230,8 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
     fe one;
     fe_one_mont(one);
     fe acc = one;
+    uint32_t live = 0;                                                  // bit g: table g has entries to convert
+    PCMM_DCHECK(batch <= 32);
     for (int g = 0; g < batch; g++) {
         const int64_t t = t0 + g * T;
         if (t >= total) break;
@@ -208,6 +239,7 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
         if (coz_chain(bsoa, plans, n, l, N, S, ptab, atab, t, one, Zf)) {
             st_xy(ptab + t * (int64_t)(kPtWords * S), acc, Zf);
             fe_mul(acc, acc, Zf);
+            live |= 1u << g;
         }
     }
 #if PCMM_TCOZ_WARPINV
@@ -216,13 +248,12 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
     fe inv = cta_inverse<false>(acc, wtot, winv);                       // 1 / (product of this thread's Zs)
 #endif
     for (int g = batch - 1; g >= 0; g--) {
+        if (!((live >> g) & 1u)) continue;
         const int64_t t = t0 + g * T;
-        if (t >= total) continue;
         const ColPlan &pl = plans[(int)((t / l) % n)];
-        if (!col_consecutive(pl, N) || pl.n[0] < 2) continue;
+        const int n1 = pl.coz;
         uint32_t *pblk = ptab + t * (int64_t)(kPtWords * S);
         uint32_t *ablk = atab + t * (int64_t)(kAffWords * S);
-        if (((ablk[kAffWords + 7] & ablk[kAffWords + 6]) == 0xffffffffu)) continue;   // identity component
         fe pre, Zf, zinv;
         ld_xy(pre, Zf, pblk);
         fe_mul(zinv, inv, pre);                                         // 1 / Z_{n1}
@@ -231,10 +262,10 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
 #if PCMM_TCOZ_PREFETCH
         // the next entry's parked (X, Y, lambda) are loaded before this entry's products (the loads'
         // L2 / HBM latency overlaps the arithmetic instead of stalling the chain)
-        fe X, Y, lam;
-        ld_xy(X, Y, pblk + pl.n[0] * kPtWords);
-        ld_x(lam, pblk + pl.n[0] * kPtWords + 16);
-        for (int u = pl.n[0]; u >= 2; u--) {
+        fe X, Y, lam = one;
+        ld_xy(X, Y, pblk + n1 * kPtWords);
+        if (n1 >= 3) ld_x(lam, pblk + n1 * kPtWords + 16);
+        for (int u = n1; u >= 2; u--) {
             fe Xn, Yn, lamn;
             if (u >= 3) {
                 const uint32_t *qn = pblk + (u - 1) * kPtWords;
@@ -246,7 +277,7 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
             fe_mul(x, X, zi2);
             fe_mul(zi3, zi2, zinv);
             fe_mul(y, Y, zi3);
-            st_xy(ablk + u * kAffWords, x, y);
+            coz_store(pl, ablk, u, x, y, S);
             if (u >= 3) {
                 fe_mul(zinv, zinv, lam);
                 X = Xn;
@@ -255,7 +286,7 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
             }
         }
 #else
-        for (int u = pl.n[0]; u >= 2; u--) {
+        for (int u = n1; u >= 2; u--) {
             const uint32_t *q = pblk + u * kPtWords;
             fe X, Y, zi2, zi3, x, y;
             ld_xy(X, Y, q);
@@ -263,7 +294,7 @@ __global__ void __launch_bounds__(128, PCMM_TCOZ_MINB)
             fe_mul(x, X, zi2);
             fe_mul(zi3, zi2, zinv);
             fe_mul(y, Y, zi3);
-            st_xy(ablk + u * kAffWords, x, y);
+            coz_store(pl, ablk, u, x, y, S);
             if (u >= 3) {
                 fe lam;
                 ld_x(lam, q + 16);

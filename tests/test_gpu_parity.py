@@ -281,6 +281,40 @@ def test_consecutive_column_tables_mixed(w, l):
     assert (_gpu_pcmm(A, ct, l, w, False, P.CUSSEN) == exp).all()
 
 
+@pytest.mark.parametrize("w,l", [(4, 128), (8, 130), (3, 128)])
+def test_signed_chain_columns_mixed(w, l):
+    # Signed A in a launch large enough for k_tables_coz (2 n l >= 65536): columns whose magnitudes are
+    # {1..M} in either sign (R10b: one chain P..MP, the entry of -v is the negated entry of
+    # v) next to columns with a gap in the magnitudes (k_tables + k_affine), only negative values,
+    # only positive values, the most negative value -2^(w-1), an all-zero column, M = 1, and identity
+    # ciphertexts in chain columns.
+    m, n = (136, 256) if w == 8 else (24, 256)
+    cfg = synth.Config("smixed", m, n, l, w, True, 0, 255, 91 + w)
+    I = synth.make_instance(cfg)
+    A = I.A.copy().astype(np.int8)
+    lo, hi = -(1 << (w - 1)), (1 << (w - 1)) - 1
+    r = np.arange(m)
+    A[:, 0] = np.where(r % 2 == 0, (r % hi) + 1, -((r % hi) + 1))       # +-1..hi mixed signs
+    A[:, 1] = -((r % min(hi, 5)) + 1)                                    # only negatives, M = min(hi, 5)
+    A[:, 2] = 0                                                          # empty column
+    A[:, 3] = np.where(r % 2 == 0, 1, -3)                                # magnitudes {1, 3}: gap -> general
+    A[:, 4] = np.where(r % 3 == 0, lo, -((r % (-lo - 1)) + 1) if lo < -1 else lo)   # includes -2^(w-1)
+    A[:, 5] = np.where(r % 2 == 0, 1, -1)                                # M = 1, both signs
+    A[:, 6] = (r % hi) + 1                                               # only positives 1..hi
+    A[:, 7] = np.where(r % 2 == 0, 2, -1)                                # {-1, 2}: magnitudes {1, 2}
+    A[:, 8] = np.where(r % 2 == 0, 3, -3)                                # {-3, 3}: gap (1, 2 missing) -> general
+    if w == 8:
+        A[:, 9] = -np.minimum(r + 1, 128)                                # -1..-128: chain of 128, all negative
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct[0, 5] = 0                                         # (inf, inf) in chain column k = 0
+    ct[7, :7, 64:] = 0                                   # C2 = inf in k = 7
+    ct[3, 2] = 0                                         # (inf, inf) in a general column
+    ct = np.ascontiguousarray(ct.reshape(n * l, 128))
+    exp, _ = oracle.pcmm(oracle.CUSSEN, A, ct, l, w)
+    assert (_gpu_pcmm(A, ct, l, w, True, P.CUSSEN) == exp).all()
+
+
 @pytest.mark.parametrize("w,signed", [(8, False), (7, True)])
 def test_xyzz_level1_tables_with_identities(w, signed):
     # k_tables_x (2^w >= 128 slots, many tables): level-2 entries made affine by a warp-shared inversion,
