@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "libpcmm.so")
 LIB_CHECKED = os.path.join(HERE, "libpcmm_checked.so")
 BUILD_CHECKED = os.path.join(HERE, "_build_checked")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-UNITS = ["hot.cu", "kernels.cu", "affine.cu", "taff.cu", "school.cu", "strassen.cu", "wide.cu", "next2.cu", "paillier.cu", "api.cu"]
+UNITS = ["hot.cu", "kernels.cu", "affine.cu", "taff.cu", "tgz.cu", "school.cu", "strassen.cu", "wide.cu", "next2.cu", "paillier.cu", "api.cu"]
 # per-unit ptxas options (measured: k_affine 256^3 0.289 -> 0.261 ms at -O1; the other units want -O3)
 UNIT_FLAGS = {"affine.cu": ["-Xptxas", "-O1"], "school.cu": ["-DPCMM_INLINE_ACCUM=0"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -458,10 +458,23 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         // (signed A: columns whose magnitudes are {1..M}, R10b; the others take k_tables + k_affine)
         const int aff = iters >= 2 && (amode == 2 || (amode == 1 && 2LL * nc * l >= 65536));
         const int fast = aff ? 2 : (tables_fast_on() && !is_signed && 2LL * nc * l >= 65536);
+        uint32_t *atables = (uint32_t *)(ws + L.scratch);
+        // general columns, fused (k_tables_gz: Alg. 2's reconstruction with an XYZZ level-1 prefix sum and
+        // the affine conversion in one kernel; no upper-level scratch): launches with enough tables to
+        // hide its two CTA-wide inversions (PCMM_TABLES_GZ: 0 never, 1 auto, 2 always; measured: 8,192 tables
+        // of w = 4 0.151 -> 0.197 ms, of w = 8 equal, 32,768 of w = 6 0.68 -> 0.61, 131,072 of w = 8 8.2 -> 6.0)
+        const int gmode = tables_gz_mode();
+        const int gz = iters >= 2 && (fast == 0 || fast == 2) &&
+                       (gmode == 2 || (gmode == 1 && 2LL * nc * l >= (L.slots >= 64 ? 8192 : 32768)));
+        if (gz) {
+            LAUNCH("tables_gz", s, launch_tables_gz(bc, pc, nc, l, iters, L.slots, L.maxup, tables, atables,
+                                                    fast == 2, status + 1, s));
+            if (fast == 2)
+                LAUNCH("tables_coz", s, launch_tables_coz(bc, pc, nc, l, iters, L.slots, tables, atables, s));
+        } else {
         LAUNCH("tables", s, launch_tables(bc, pc, nc, l, iters, L.slots, L.maxup, is_signed, tables,
                                           (uint32_t *)(ws + L.scratch), s, fast != 0, std::min(m, L.slots - 1),
                                           status + 1));
-        uint32_t *atables = (uint32_t *)(ws + L.scratch);
         // after k_tables: the affine tables share the region of k_tables' upper-level scratch
         if (fast == 2) {
             LAUNCH("tables_coz", s, launch_tables_coz(bc, pc, nc, l, iters, L.slots, tables, atables, s));
@@ -470,6 +483,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         }
         LAUNCH("affine", s, launch_affine(tables, 2LL * nc * l * L.slots, atables, s, pc, nc, l, L.slots, iters, fast,
                                           status + 1));
+        }
         // chunked: when one chunk's accumulation alone fills the GPU (>= 2 waves of CTAs), no split-k --
         // each chunk adds straight into the running output (the accumulators start from it: 3 + 3
         // products per output and chunk instead of a k_reduce pass with a complete addition per split)

@@ -67,7 +67,13 @@ cudaError_t launch_tables_fast(const uint32_t *bsoa, const ColPlan *plans, int n
 // tables: the projective table region (per-entry X, Y, lambda parked there)
 cudaError_t launch_tables_coz(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots,
                               uint32_t *tables, uint32_t *atables, cudaStream_t s);
-int tables_coz_mode();   // PCMM_TABLES_COZ: 0 off, 1 auto (default), 2 always (unsigned A)
+int tables_coz_mode();   // PCMM_TABLES_COZ: 0 off, 1 auto (default), 2 always
+// general columns, tables and affine conversion in one kernel (tgz.cu k_tables_gz); skip_chain:
+// chain columns are left to k_tables_coz.  tables: the projective region (X, Y, f parked per entry)
+cudaError_t launch_tables_gz(const uint32_t *bsoa, const ColPlan *plans, int n, int l, int N, int slots, int maxup,
+                             uint32_t *tables, uint32_t *atables, int skip_chain, const int *general,
+                             cudaStream_t s);
+int tables_gz_mode();    // PCMM_TABLES_GZ: 0 off (k_tables + k_affine), 1 auto (default), 2 always
 // upper-level reconstruction scratch per (c, k, j): two ping-pong levels of
 // kMaxUpper entries (levels >= 2 have <= 7 entries for w <= 4, <= 28 for w <= 8)
 inline int max_upper(int w) { return w <= 4 ? 8 : 32; }

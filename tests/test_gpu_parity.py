@@ -812,6 +812,42 @@ def test_consecutive_table_kernels_forced(mode):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("m,n,l,w,signed", [(64, 128, 128, 4, False), (48, 128, 128, 6, True), (40, 64, 64, 8, False)])
+def test_general_fused_tables_every_output(m, n, l, w, signed):
+    # launches of the size at which the default picks k_tables_gz (32,768 tables; 8,192 of 2^w >= 64
+    # slots) but not k_tables_coz: every column, chain columns included, goes through the fused
+    # general kernel (doubling steps T[2] = P + P, gaps, signed level sets); identity ciphertexts and
+    # a repeated ciphertext in the inputs; every output against the oracle
+    cfg = synth.Config("gz", m, n, l, w, signed, 0, 255, 500 + w)
+    I = synth.make_instance(cfg)
+    x = synth.keygen_secret(cfg.seed)
+    ct = oracle.encrypt(ecref.mulG(x), I.B.reshape(-1), I.r_be).reshape(n, l, 128)
+    ct[3, 2] = 0                                         # (inf, inf)
+    ct[5, :4, :64] = 0                                   # C1 = inf
+    ct[7] = ct[6]                                        # equal ciphertexts in consecutive k
+    ct = np.ascontiguousarray(ct.reshape(n * l, 128))
+    exp, _ = oracle.pcmm(oracle.CUSSEN, I.A, ct, l, w)
+    assert (_gpu_pcmm(I.A, ct, l, w, signed, P.CUSSEN) == exp).all()
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_general_table_kernels_forced(mode):
+    # PCMM_TABLES_GZ=2: the fused general-column kernel (k_tables_gz: XYZZ level-1 prefix sum with the
+    # affine conversion, doubling steps, identity components) for every launch, also the small ones;
+    # 0: k_tables / k_tables_x + k_affine everywhere (the default picks by launch size)
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_TABLES_GZ=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or "
+                        "test_consecutive_column or test_signed_chain or test_xyzz_level1 or test_all_identity or "
+                        "test_extreme_values or test_vector_times or test_accumulator_exceptional"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_xyzz_schoolbook_forced():
     # the XYZZ schoolbook kernel (school.cu, PCMM_SCHOOL_XYZZ=1) on the every-output cases, including the
     # exceptional accumulator cases (equal and opposite terms) and identity ciphertexts
