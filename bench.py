@@ -467,12 +467,13 @@ class Problem:
                                        "numerator": "SURVEY.md §8(d) F = 14 (useful adds) + 13 (doublings) "
                                                     f"+ 6 (points) = {W['F_step']:.4g} fp_mul"}}
         if self.path == P.CUSSEN and "accum" in kern:
-            t_acc = kern["accum"]["ms_per_step"] + kern.get("reduce", {"ms_per_step": 0})["ms_per_step"]
+            t_acc = (kern["accum"]["ms_per_step"] + kern.get("reduce", {"ms_per_step": 0})["ms_per_step"] +
+                     kern.get("rowperm", {"ms_per_step": 0})["ms_per_step"])
             ach = W["F_accum"] / (t_acc * 1e-3) / 1e9
             ex = W["exec_accum"] / (t_acc * 1e-3) / 1e9
             traffic, tsrc = dram_traffic(cfg.name)
             res["roofline"] = {
-                "bound": "alu", "kernel": "k_accum (+k_reduce)", "achieved": ach, "peak": g.peak,
+                "bound": "alu", "kernel": ("k_accum_g2 (+k_rowperm, k_reduce)" if "rowperm" in kern else "k_accum (+k_reduce)"), "achieved": ach, "peak": g.peak,
                 "unit": "G fp_mul/s", "frac": ach / g.peak, "traffic": traffic, "traffic_source": tsrc,
                 "frac_executed_products": ex / g.peak,
                 "frac_vs_r01_peak": ach / (g.peak * P_PROD_K11 / P_PROD),

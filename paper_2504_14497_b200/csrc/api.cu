@@ -55,7 +55,7 @@ std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- workspace
 struct Layout {
-    size_t status = 0, bsoa = 0, plans = 0, rank = 0, tables = 0, scratch = 0, partial = 0, bsoa_c = 0, total = 0;
+    size_t status = 0, bsoa = 0, plans = 0, rank = 0, perm = 0, tables = 0, scratch = 0, partial = 0, bsoa_c = 0, total = 0;
     int rows = 128, ksplit = 1, slots = 16, maxup = 8;
     int kc = 0;                            // inner indices per table chunk (= n: one chunk)
 };
@@ -121,7 +121,8 @@ Layout layout(int m, int n, int l, int w, int path) {
         // kChunkSplits partial sums and the chunk's imported rows
         const size_t per_k = byte_table_bytes_per_k(l, w);
         const size_t slot = 2 * (size_t)kPtWords * 4 * (size_t)m * l;     // one set of partial sums
-        const size_t fixed0 = off + align256((size_t)n * sizeof(ColPlan)) + align256((size_t)n * m) + 4096;
+        const size_t fixed0 = off + align256((size_t)n * sizeof(ColPlan)) + align256((size_t)n * m) +
+                              align256((size_t)16 * ((m + 127) / 128) * 128 * 4) + 4096;
         const int ks_full = choose_ksplit(m, n, l, w);
         int kc = n;
         if (fixed0 + (ks_full > 1 ? ks_full * slot : 0) + (size_t)n * per_k > byte_budget()) {
@@ -140,6 +141,8 @@ Layout layout(int m, int n, int l, int w, int path) {
         off = align256(off + (size_t)n * sizeof(ColPlan));
         L.rank = off;
         off = align256(off + (size_t)n * m);
+        L.perm = off;                      // k_rowperm: up to 16 splits x 128-row blocks x 128 ints
+        off = align256(off + (size_t)16 * ((m + 127) / 128) * 128 * 4);
         const size_t ccnt = (size_t)kc * l;
         L.tables = off;
         off = align256(off + ccnt * 2 * (size_t)kPtWords * L.slots * 4);
@@ -499,7 +502,21 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
         uint32_t *acc_out = direct ? out : (uint32_t *)(ws + L.partial);
         const int64_t split_stride = direct ? 0 : 2LL * kPtWords * cnt;
         const int acc_in = direct && chunked && k0 > 0;
-        if (w <= 4) {
+        // PCMM_ACC_MODE: 0 = k_accum (tables staged in shared memory, w <= 4) / k_accum_g (w > 4);
+        // 1 = k_accum_g (gather) for every w; 2 = k_rowperm + k_accum_g2 (gather, rows sorted by nonzero
+        // count, 4-group step); 3 (default) = the same with the software-pipelined step.  m <= 64 keeps mode 0.
+        static int acc_mode = -1;
+        if (acc_mode < 0) {
+            const char *e = getenv("PCMM_ACC_MODE");
+            acc_mode = e ? atoi(e) : 3;       // measured (256^3 / 512^3 / ML step): mode 0 4.157 / 24.23 / 2.230 ms,
+                                              // 1: 4.185 / 25.13 / 2.270, 2: 4.131 / 24.05 / 2.227, 3: 3.979 / 23.14 / 2.152
+        }
+        if (acc_mode >= 2 && ks <= 16 && m > 64) {
+            int *perm = (int *)(ws + L.perm);
+            LAUNCH("rowperm", s, launch_rowperm(rc_, m, nc, ks, perm, s));
+            LAUNCH("accum", s, launch_accum_sorted(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in,
+                                                   perm, acc_mode == 3));
+        } else if (w <= 4 && acc_mode == 0) {
             LAUNCH("accum", s, launch_accum(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in));
         } else {
             LAUNCH("accum", s,

@@ -288,6 +288,119 @@ __global__ void __launch_bounds__(kRowsG, 3)
     soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
 }
 
+// ------------------------------------------------------------ a4, gather kernel with sorted rows
+// Every lane skips its own zero entries (a_ik = 0 adds the identity, R1), so a warp runs the
+// maximum over its lanes of the nonzero count: with rows in matrix order that is 6 % (256^3, 1/16
+// zeros) to 10 % (512^3, w = 2: 1/4 zeros) more steps than the mean.  k_rowperm sorts the rows of
+// each 128-row block by their nonzero count over the k-range of each split (the permutation serves
+// every output column j and both components), so the lanes of a warp finish together; k_accum_g2 is
+// k_accum_g with the row of a thread taken from that permutation and the software-pipelined step
+// (jac.cuh xyzz_add_aff_pipe).  Which output a thread accumulates changes; what it adds does not.
+__global__ void __launch_bounds__(kRowsG) k_rowperm(const uint8_t *__restrict__ rank, int m, int n, int ksplit,
+                                                    int *__restrict__ perm) {
+    __shared__ uint32_t key[kRowsG];
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const int rb = (int)blockIdx.x % rowblocks, s = (int)blockIdx.x / rowblocks;
+    const int tid = (int)threadIdx.x;
+    const int i = rb * kRowsG + tid;
+    const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
+    uint32_t cnt = 0;
+    if (i < m)
+        for (int k = kb; k < ke; k++) cnt += rank[(int64_t)k * m + i] != 0;
+    PCMM_DCHECK(cnt < (1u << 24));
+    key[tid] = (cnt << 8) | (uint32_t)tid;                  // rows >= m: count 0, sorted last
+    __syncthreads();
+    for (int size = 2; size <= kRowsG; size <<= 1) {        // bitonic sort, descending
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int p = tid ^ stride;
+            if (p > tid) {
+                const uint32_t a = key[tid], b = key[p];
+                const bool desc = (tid & size) == 0;
+                if (desc ? a < b : a > b) {
+                    key[tid] = b;
+                    key[p] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    perm[((int64_t)s * rowblocks + rb) * kRowsG + tid] = rb * kRowsG + (int)(key[tid] & 0xffu);
+}
+
+template <bool kPipe>
+__global__ void __launch_bounds__(kRowsG, 3)
+    k_accum_g2(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int S,
+               int ksplit, uint32_t *__restrict__ out, int64_t split_stride, int acc_in,
+               const int *__restrict__ perm) {
+    int b = blockIdx.x;
+    const int j = b % l; b /= l;
+    const int c = b & 1; b >>= 1;
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const int rb = b % rowblocks;
+    const int s = b / rowblocks;
+    const int i = perm[((int64_t)s * rowblocks + rb) * kRowsG + (int)threadIdx.x];
+    PCMM_DCHECK(i >= rb * kRowsG && i < (rb + 1) * kRowsG);
+    if (i >= m) return;
+    const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
+    const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive k
+    const uint32_t *tb = tables + (((int64_t)c * n) * l + j) * (int64_t)S * kAffWords;
+    acc_t acc;
+    acc_init(acc);
+    if (acc_in) acc_load_running(acc, out + (int64_t)c * kPtWords * m * l, (int64_t)m * l, (int64_t)i * l + j);
+    int k = kb;
+    while (k < ke && rank[(int64_t)k * m + i] == 0) k++;
+    if (k < ke) {
+        fe x2, y2;
+        PCMM_DCHECK(rank[(int64_t)k * m + i] < S);
+        load_aff(x2, y2, tb + k * tstride + rank[(int64_t)k * m + i] * kAffWords);
+#if PCMM_ACC_XYZZ
+        fe U2;
+        bool have_u2 = false;
+#endif
+        while (true) {
+            int kn = k + 1;
+            while (kn < ke && rank[(int64_t)kn * m + i] == 0) kn++;
+            fe xn = x2, yn = y2;
+            PCMM_DCHECK(kn >= ke || rank[(int64_t)kn * m + i] < S);
+            if (kn < ke) load_aff(xn, yn, tb + kn * tstride + rank[(int64_t)kn * m + i] * kAffWords);
+#if PCMM_ACC_XYZZ
+            if (kPipe) xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);
+            else acc_add_aff(acc, x2, y2);
+#else
+            acc_add_aff(acc, x2, y2);
+#endif
+            if (kn >= ke) break;
+            x2 = xn;
+            y2 = yn;
+            k = kn;
+        }
+    }
+    const int64_t cnt = (int64_t)m * l;
+    pt o;
+    acc_to_proj(o, acc);
+    soa_store_hot(out + (int64_t)s * split_stride + (int64_t)c * kPtWords * cnt, cnt, (int64_t)i * l + j, o);
+}
+
+cudaError_t launch_rowperm(const uint8_t *rank, int m, int n, int ksplit, int *perm, cudaStream_t s) {
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    k_rowperm<<<(unsigned)(rowblocks * ksplit), kRowsG, 0, s>>>(rank, m, n, ksplit, perm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_accum_sorted(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in,
+                                const int *perm, int pipe) {
+    const int rowblocks = (m + kRowsG - 1) / kRowsG;
+    const unsigned grid = (unsigned)((int64_t)l * 2 * rowblocks * ksplit);
+    if (pipe)
+        k_accum_g2<true><<<grid, kRowsG, 0, s>>>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, acc_in,
+                                                 perm);
+    else
+        k_accum_g2<false><<<grid, kRowsG, 0, s>>>(tables, rank, m, n, l, slots, ksplit, out, out_stride_split, acc_in,
+                                                  perm);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ a4 (wide path, NEXT-1): one k-chunk
 // As k_accum_g for the chunk k0 .. k0+kc-1 of the wide path (wide.cu): uint16
 // rank, tables [c][kk][j][slot][16].  The accumulator starts from the running

@@ -81,6 +81,12 @@ inline int max_upper(int w) { return w <= 4 ? 8 : 32; }
 cudaError_t launch_accum_global(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
                                 int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in = 0);
 int accum_global_ctas_per_sm();
+// rows of every 128-row block sorted by nonzero count per k-split (perm: ksplit x ceil(m/128) x 128 ints),
+// and the gather accumulate kernel that takes its rows from that permutation (hot.cu k_rowperm, k_accum_g2)
+cudaError_t launch_rowperm(const uint8_t *rank, int m, int n, int ksplit, int *perm, cudaStream_t s);
+cudaError_t launch_accum_sorted(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots,
+                                int ksplit, uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in,
+                                const int *perm, int pipe);
 cudaError_t launch_accum(const uint32_t *tables, const uint8_t *rank, int m, int n, int l, int slots, int ksplit,
                          uint32_t *out, int64_t out_stride_split, cudaStream_t s, int acc_in = 0);
 // out = sum of the ksplit partial sums (+ out itself when accumulate: the byte path's k-chunks)
