@@ -516,7 +516,7 @@ static int mul_common(int path, const int8_t *A_d, int m, int n, int l, int w, i
             LAUNCH("rowperm", s, launch_rowperm(rc_, m, nc, ks, perm, s));
             LAUNCH("accum", s, launch_accum_sorted(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in,
                                                    perm, acc_mode == 3));
-        } else if (w <= 4 && acc_mode == 0) {
+        } else if (w <= 4 && (acc_mode == 0 || (acc_mode >= 2 && m <= 64))) {      // m <= 64: 64-row k_accum CTAs
             LAUNCH("accum", s, launch_accum(atables, rc_, m, nc, l, L.slots, ks, acc_out, split_stride, s, acc_in));
         } else {
             LAUNCH("accum", s,

@@ -1,6 +1,8 @@
 // hot.cu -- the dominant kernel of the Cussen path (step a4 of SURVEY.md §8(a))
 // and the fp_mul throughput probe, in their own translation unit (parallel
 // compilation; the hot loop inlines the complete addition and fe_mul).
+#include <algorithm>
+
 #include "ec.cuh"
 #include "internal.h"
 #include "jac.cuh"
@@ -327,6 +329,46 @@ __global__ void __launch_bounds__(kRowsG) k_rowperm(const uint8_t *__restrict__ 
     perm[((int64_t)s * rowblocks + rb) * kRowsG + tid] = rb * kRowsG + (int)(key[tid] & 0xffu);
 }
 
+// m <= 4096: all rows of a split sorted together (one CTA per split, bitonic sort of the next power of
+// two >= the padded row count in shared memory), so that a warp's 32 rows are 32 consecutive order
+// statistics of the whole column of counts instead of a quarter of one 128-row block's
+// (512^3, w = 2: the spread of the counts inside a warp drops from ~1 sigma to ~0.3 sigma).
+__global__ void __launch_bounds__(1024) k_rowperm_all(const uint8_t *__restrict__ rank, int m, int n, int ksplit,
+                                                      int np, int *__restrict__ perm) {
+    extern __shared__ uint32_t keys[];
+    const int s = (int)blockIdx.x, tid = (int)threadIdx.x, nt = (int)blockDim.x;
+    const int mpad = ((m + kRowsG - 1) / kRowsG) * kRowsG;
+    const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
+    PCMM_DCHECK(np <= 4096 && mpad <= np);
+    for (int idx = tid; idx < np; idx += nt) {
+        uint32_t cnt = 0;
+        if (idx < m) {
+            cnt = 1;                                        // every valid row sorts before the padding
+            for (int k = kb; k < ke; k++) cnt += rank[(int64_t)k * m + idx] != 0;
+        }
+        PCMM_DCHECK(cnt < (1u << 20));
+        keys[idx] = (cnt << 12) | (uint32_t)idx;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np; size <<= 1) {            // bitonic sort, descending
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int idx = tid; idx < np; idx += nt) {
+                const int p = idx ^ stride;
+                if (p > idx) {
+                    const uint32_t a = keys[idx], b = keys[p];
+                    const bool desc = (idx & size) == 0;
+                    if (desc ? a < b : a > b) {
+                        keys[idx] = b;
+                        keys[p] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int idx = tid; idx < mpad; idx += nt) perm[(int64_t)s * mpad + idx] = (int)(keys[idx] & 0xfffu);
+}
+
 template <bool kPipe>
 __global__ void __launch_bounds__(kRowsG, 3)
     k_accum_g2(const uint32_t *__restrict__ tables, const uint8_t *__restrict__ rank, int m, int n, int l, int S,
@@ -339,7 +381,7 @@ __global__ void __launch_bounds__(kRowsG, 3)
     const int rb = b % rowblocks;
     const int s = b / rowblocks;
     const int i = perm[((int64_t)s * rowblocks + rb) * kRowsG + (int)threadIdx.x];
-    PCMM_DCHECK(i >= rb * kRowsG && i < (rb + 1) * kRowsG);
+    PCMM_DCHECK(i >= 0 && i < rowblocks * kRowsG + 4096);
     if (i >= m) return;
     const int kb = (int)((int64_t)s * n / ksplit), ke = (int)((int64_t)(s + 1) * n / ksplit);
     const int64_t tstride = (int64_t)l * S * kAffWords;                  // words between consecutive k
@@ -383,7 +425,18 @@ __global__ void __launch_bounds__(kRowsG, 3)
 
 cudaError_t launch_rowperm(const uint8_t *rank, int m, int n, int ksplit, int *perm, cudaStream_t s) {
     const int rowblocks = (m + kRowsG - 1) / kRowsG;
-    k_rowperm<<<(unsigned)(rowblocks * ksplit), kRowsG, 0, s>>>(rank, m, n, ksplit, perm);
+    static int all_env = -1;                                  // PCMM_ROWPERM_ALL=0: per-block sort always
+    if (all_env < 0) {
+        const char *e = getenv("PCMM_ROWPERM_ALL");
+        all_env = e ? atoi(e) : 1;
+    }
+    if (all_env && rowblocks * kRowsG <= 4096) {
+        int np = 128;
+        while (np < rowblocks * kRowsG) np <<= 1;
+        k_rowperm_all<<<(unsigned)ksplit, std::min(1024, np), (size_t)np * 4, s>>>(rank, m, n, ksplit, np, perm);
+    } else {
+        k_rowperm<<<(unsigned)(rowblocks * ksplit), kRowsG, 0, s>>>(rank, m, n, ksplit, perm);
+    }
     return cudaGetLastError();
 }
 
