@@ -492,12 +492,20 @@ __global__ void __launch_bounds__(kRowsG, 3)
     if (k < kc) {
         fe x2, y2;
         load_aff(x2, y2, tb + k * tstride + (int64_t)rk[(int64_t)k * m] * kAffWords);
+#if PCMM_ACC_XYZZ
+        fe U2;
+        bool have_u2 = false;
+#endif
         while (true) {
             int kn = k + 1;
             while (kn < kc && rk[(int64_t)kn * m] == 0) kn++;
-            fe xn, yn;
+            fe xn = x2, yn = y2;
             if (kn < kc) load_aff(xn, yn, tb + kn * tstride + (int64_t)rk[(int64_t)kn * m] * kAffWords);
+#if PCMM_ACC_XYZZ
+            xyzz_add_aff_pipe(acc, x2, y2, U2, have_u2, xn);          // the software-pipelined step (as k_accum_g2)
+#else
             acc_add_aff(acc, x2, y2);
+#endif
             if (kn >= kc) break;
             x2 = xn;
             y2 = yn;

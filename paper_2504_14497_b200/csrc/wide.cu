@@ -176,6 +176,11 @@ __device__ __forceinline__ void ws_load(pt &q, const uint32_t *scr, int64_t base
     }
 }
 
+#ifndef PCMM_WIDE_SHARED_DBL
+#define PCMM_WIDE_SHARED_DBL 1      // level-N ECSMs of k_tables_wide with shared doublings (0: one binary ECSM per value)
+#endif
+constexpr bool kWideSharedDbl = PCMM_WIDE_SHARED_DBL != 0;
+
 __global__ void __launch_bounds__(128, 3) k_tables_wide(const uint32_t *__restrict__ bsoa,
                                                         const int32_t *__restrict__ pn,
                                                         const int32_t *__restrict__ psN,
@@ -211,10 +216,44 @@ __global__ void __launch_bounds__(128, 3) k_tables_wide(const uint32_t *__restri
     } else {
         int src = 0;
         const int nN = nl[N - 1];
+        // Alg. 3 l.5: the level-N ECSMs s^(N)[u] P all multiply the same point, so the doublings are
+        // shared: D[i] = 2^i P once (nb - 1 doublings), then v P = the sum of the D[i] of v's set bits
+        // (popcount - 1 complete additions instead of nb - 1 doublings + popcount - 1 additions per value;
+        // t = 16, 256 rows: ~250 values per column, 24 -> 8 point operations each)
+        unsigned maxmag = 0;
         for (int u = 0; u < nN; u++) {
-            pt e;
-            pt_mul_small_g<MulCall>(e, sN[u], P);                           // Alg. 3 l.5
-            ws_store(sj, sbase, src + u, l, e);
+            const int v = sN[u];
+            maxmag = max(maxmag, v < 0 ? (unsigned)(-v) : (unsigned)v);
+        }
+        int nb = 0;
+        while (nb < 32 && (maxmag >> nb)) nb++;
+        constexpr int kMaxBits = 20;
+        if (kWideSharedDbl && nN >= 3 && nb <= kMaxBits) {
+            pt D[kMaxBits];
+            D[0] = P;
+            for (int i = 1; i < nb; i++) pt_dbl_pair(D[i], D[i - 1]);
+            for (int u = 0; u < nN; u++) {
+                const int v = sN[u];
+                unsigned a = v < 0 ? (unsigned)(-v) : (unsigned)v;
+                pt e;
+                pt_identity(e);
+                bool first = true;
+                for (int i = 0; i < nb; i++) {
+                    if ((a >> i) & 1u) {
+                        if (first) e = D[i];
+                        else pt_add_pair(e, e, D[i]);
+                        first = false;
+                    }
+                }
+                if (v < 0) pt_neg(e, e);
+                ws_store(sj, sbase, src + u, l, e);
+            }
+        } else {
+            for (int u = 0; u < nN; u++) {
+                pt e;
+                pt_mul_small_g<MulCall>(e, sN[u], P);                       // Alg. 3 l.5
+                ws_store(sj, sbase, src + u, l, e);
+            }
         }
         for (int lev = N - 1; lev >= 2; lev--) {                            // prefix sums, levels N-1 .. 2
             const int dst = cap - src;
