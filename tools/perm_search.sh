@@ -12,7 +12,7 @@ C=paper_2504_14497_b200/csrc
 build_one() {
   name=$1; shift
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC,-fvisibility=hidden -I include "$@" -c $C/hot.cu -o /tmp/perm/$name.o && \
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o abv/$name.so /tmp/perm/$name.o $B/kernels.o $B/affine.o $B/taff.o $B/school.o $B/strassen.o $B/wide.o $B/next2.o $B/paillier.o $B/api.o
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o abv/$name.so /tmp/perm/$name.o $B/kernels.o $B/affine.o $B/taff.o $B/tgz.o $B/school.o $B/strassen.o $B/wide.o $B/next2.o $B/paillier.o $B/api.o
 }
 n=0
 while read -r name flags; do
