@@ -522,7 +522,9 @@ def test_empty_and_invalid_sizes():
 
 def test_extreme_values_and_shapes():
     # extreme plaintexts (all max / all min signed), many rows (16 row blocks), long k (split-k)
-    for (m, n, l, w, signed) in ((2048, 6, 2, 4, False), (40, 2048, 2, 4, True), (16, 8, 3, 8, True)):
+    # (m = 4200 > 4096: k_rowperm sorts per 128-row block instead of the whole column, 33 row blocks, ragged tail)
+    for (m, n, l, w, signed) in ((2048, 6, 2, 4, False), (40, 2048, 2, 4, True), (16, 8, 3, 8, True),
+                                 (4200, 7, 2, 3, False)):
         cfg = synth.Config("edge", m, n, l, w, signed, 0, 255, 31 + m)
         I = synth.make_instance(cfg)
         lo, hi = cfg.a_range
@@ -843,6 +845,21 @@ def test_general_table_kernels_forced(mode):
                         "test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or "
                         "test_consecutive_column or test_signed_chain or test_xyzz_level1 or test_all_identity or "
                         "test_extreme_values or test_vector_times or test_accumulator_exceptional"],
+                       env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_rowperm_per_block_forced():
+    # PCMM_ROWPERM_ALL=0: rows sorted inside each 128-row block (the path of m > 4096) on the every-output
+    # cases with m > 64, incl. 256^3 and 512^3
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PCMM_ROWPERM_ALL="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_ragged_shapes or test_full_size_cussen_every_output or test_extreme_values or "
+                        "test_signed_chain or test_byte_path_k_chunks"],
                        env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
