@@ -1,3 +1,4 @@
+# GPU-box job: parity tests under PCMM_ACC_MODE=2, 3 and the accumulate modes' timing (DESIGN.md section 6 table)
 mkdir -p gpurun_out
 for mode in 2 3; do
 PCMM_ACC_MODE=$mode timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "ragged or accumulator_exceptional or full_size_cussen or degenerate or signed_chain or general_fused or extreme" > gpurun_out/t_acc$mode.log 2>&1
