@@ -128,10 +128,12 @@ PCMM_API int pcmm_mul_schoolbook(const int8_t *A_d, int m, int n, int l, int w, 
  *   a3  reconstruction prefix sums (Alg. 2 lines 14-23) build the table
  *       T_kj[v] = v * Enc(b_kj) for the distinct values v of A[:,k];
  *   a4  un-sort / re-insert + accumulation (Alg. 3 lines 6-9): every output
- *       gathers C_ij += T_kj[a_ik] from shared-memory table chunks.
+ *       gathers C_ij += T_kj[a_ik] from the affine tables (L1/L2-resident;
+ *       m <= 64 and w <= 4: from table chunks staged in shared memory).
  * Output identical (after pcmm_normalize) to pcmm_mul_schoolbook.
- * w in [1, 8] (tables of <= 2^w - 1 entries per (k, j): w <= 4 staged in
- * shared memory, w > 4 gathered from L2-resident global tables).  Async.
+ * w in [1, 8] (tables of <= 2^w - 1 entries per (k, j)).  Signed A: a column
+ * whose magnitudes are {1..M} gets the entry of -v as the negation of the
+ * entry of v (R10b); the outputs do not depend on it.  Async.
  * Errors as pcmm_mul_schoolbook; ENOTSUP for iters outside [1, 4].        */
 PCMM_API int pcmm_mul_cussen(const int8_t *A_d, int m, int n, int l, int w, int is_signed, int iters, const uint8_t *ctB_d,
                     void *ctC_proj_d, void *ws_d, size_t ws_bytes, void *stream);
