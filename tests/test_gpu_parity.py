@@ -947,9 +947,9 @@ def test_c512_w8_chunked_sampled():
 
 def test_checked_build():
     # the device bounds-check build (libpcmm_checked.so, PCMM_CHECKED=1: shared-memory staging and scans,
-    # table slots, scratch entries, plan bitmaps, CTA-inverse layout) on the every-output cases and the
-    # forced variants (block scans, consecutive-table kernels, k-chunks, XYZZ schoolbook); a failed
-    # check traps the launch.  Stands in for compute-sanitizer memcheck, which the GPU pool does not run.
+    # table slots, scratch entries, plan bitmaps, CTA-inverse layout, chain-column slots, the row
+    # permutation) on the every-output cases incl. the signed chain columns, the fused general-column
+    # kernel and the k-chunked byte path; a failed check traps the launch.  Stands in for compute-sanitizer memcheck, which the GPU pool does not run.
     import os
     import subprocess
     import sys
@@ -958,7 +958,8 @@ def test_checked_build():
                         "(test_ragged_shapes or test_tiny or test_c64_config or test_degenerate or test_consecutive_column "
                         "or test_all_identity or test_accumulator_exceptional or test_xyzz_level1 or test_vector "
                         "or test_wide_every_output or test_wide_chunked or test_strassen_every or test_plan_matches "
-                        "or test_extreme_values or test_forced or test_byte_path_k_chunks or test_paillier_every "
+                        "or test_extreme_values or test_byte_path_k_chunks or test_paillier_every "
+                        "or test_signed_chain or test_general_fused "
                         "or test_full_size_comparison_paths_sampled or test_c512_w8_chunked_sampled "
                         "or test_full_size_gpu_encrypted_inputs_sampled or test_wide_full_grid_size_sampled) "
                         "and not test_checked_build"],
