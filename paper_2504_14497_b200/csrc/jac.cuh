@@ -193,16 +193,19 @@ __device__ __forceinline__ void jac_dbl(jacc &A) {
 // Z3 = Z1 H).  Same exceptional cases as jac_add_aff (identity, P = 0), which
 // take the complete RCB16 path on homogeneous images.
 #ifndef PCMM_ACC_PERM
-#define PCMM_ACC_PERM 0         // 1: product order / operand order of the pipelined step from PCMM_G1, _G2, _G3, _SWAPM
+// 1 (default): product order / operand order of the pipelined step from PCMM_G1, _G2, _G3, _SWAPM;
+// 0: the grouped calls in their original order.  Measured with k_accum_g2 (256^3 / 512^3 / ML step):
+// 0: 3.960 / 22.69 / 2.156 ms; 1 with the orders below: 3.930 / 22.34 / 2.145
+#define PCMM_ACC_PERM 1
 #endif
 #ifndef PCMM_G1
 #define PCMM_G1 12
 #endif
 #ifndef PCMM_G2
-#define PCMM_G2 1234
+#define PCMM_G2 2341            // PPP, Q, ZZ3, R^2
 #endif
 #ifndef PCMM_G3
-#define PCMM_G3 1234
+#define PCMM_G3 4123            // U2', R (Q - X3), Y PPP, ZZZ3
 #endif
 #ifndef PCMM_SWAPM
 #define PCMM_SWAPM 0
